@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""Benchmark of the batched env step (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5]
+    python bench.py --impl reference ...       # the reference arm (CPU oracle port)
+
+Workload (default ``c2`` = BASELINE.json configs[1]): BlueROV2 station-keeping,
+4,096 envs per GPU, seed 0, fixed U[-1,1] bench actions (reference
+batch.py:168-197), synthetic, one CUDA-graph-replayed fused step per timed
+step.  Timing: W warm-up steps, then K steps, each bracketed by CUDA events on
+the launching stream with an L2 flush (256 MiB write) between steps; barrier +
+synchronize on both sides; max over ranks.  ``value`` = env-steps/s of the
+whole job with inputs resident in HBM; ``e2e`` = the same metric through the
+reference-facing C ABI (``uuvsim_step`` with pinned host f64 buffers, H2D of
+actions and D2H of obs/reward/done inside the timed region).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONTROL_DT = 0.05
+# Algorithmic flops per env-step of the reference path (counted on
+# the reference's flat kernels for the 8-thruster Heavy; each thruster fewer
+# removes its thrust curve (2) and allocation column (12) = 14 flop).
+FLOPS_8THR = {"station_keeping": 4073, "circle": 4157, "helix": 4169, "lemniscate": 4181}
+L2_FLUSH_BYTES = 256 << 20
+
+CONFIGS = {
+    "c2": dict(workload="C2 BlueROV2 station-keeping, 4096 envs/GPU", kind="station_keeping",
+               vehicles=["bluerov2"], num_envs=4096, dr=None),
+    "c3": dict(workload="C3 BlueROV2-Heavy lemniscate tracking + per-episode DR, 65536 envs/GPU",
+               kind="lemniscate", vehicles=["bluerov2_heavy"], num_envs=65536, dr="episode"),
+    "c4": dict(workload="C4 BlueROV2 circle tracking, 16384 envs/GPU", kind="circle",
+               vehicles=["bluerov2"], num_envs=16384, dr=None),
+    "c5": dict(workload="C5 mixed BlueROV2/Heavy station-keeping, 1048576 envs/GPU",
+               kind="station_keeping", vehicles=["bluerov2_heavy", "bluerov2"],
+               num_envs=1 << 20, dr=None),
+}
+
+
+def flops_per_env_step(kind: str, n_thr_list) -> float:
+    n = float(np.mean(n_thr_list))
+    return FLOPS_8THR[kind] - 14.0 * (8.0 - n)
+
+
+def bytes_per_env_step(kind: str, n_act: int, obs_dim: int, dr: bool) -> int:
+    """Minimum HBM bytes per env-step of the fp32 device path."""
+    b = 48 * 2            # state read + write (12 fp32)
+    b += 4 * n_act        # actions
+    b += 4 * obs_dim      # observation
+    b += 4 + 1 + 1        # reward, done, reason
+    b += 4 * 2            # step counter read + write
+    b += 4 * 2            # running episode return read + write
+    if dr:
+        b += 40           # randomised parameter record (10 fp32)
+    if kind != "station_keeping":
+        pass              # trajectory table is a few KB, L1/L2 resident
+    return b
+
+
+def build_config(name: str, rank: int, precision: str):
+    import paper_2410_14117_b200 as uuv
+    c = CONFIGS[name]
+    n = c["num_envs"]
+    spec = uuv.TaskSpec(kind=c["kind"])
+    ranges = uuv.default_ranges(per_episode=True) if c["dr"] == "episode" else None
+    vdocs = [uuv.VehicleParams(uuv.vehicles.get_vehicle(v)) for v in c["vehicles"]]
+    if len(vdocs) > 1:
+        # global 50/50 mix over the whole job, contiguous slabs (per-env vehicle id)
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        total = n * world
+        cfg = uuv.engine_config_dict(vdocs, spec, n, 0, 0, ranges, precision=precision,
+                                     device=rank_device(), env_offset=rank * n,
+                                     vehicle_mix=[total // 2, total - total // 2])
+    else:
+        cfg = uuv.engine_config_dict(vdocs[0], spec, n, 0, 0, ranges, precision=precision,
+                                     device=rank_device(), env_offset=rank * n)
+    return cfg, [v.n_thrusters() for v in vdocs]
+
+
+def rank_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"uuv_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.is_file():
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.is_file():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6551.7)), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+def profile_traffic(config: str):
+    """dram bytes per launch of the step kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.is_file():
+        d = json.loads(p.read_text())
+        return d.get(config)
+    return None
+
+
+# --------------------------------------------------------------------------- CPU arm
+def cpu_oracle_run(cfg: dict, n_steps_cap: int, seconds: float, threads: int):
+    """Time the oracle port (uuv_oracle.c) on host cores over a bounded sample."""
+    from oracle import oracle as orc
+    b = orc.OracleBatch(cfg, threads=threads)
+    act = orc.bench_actions(cfg["seed"], b.num_envs, b.action_dim)
+    b.step(act)   # warm
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < n_steps_cap and (time.perf_counter() - t0) < seconds:
+        b.step(act)
+        steps += 1
+    wall = time.perf_counter() - t0
+    b.close()
+    return b.num_envs * steps / wall, steps, wall
+
+
+def cpu_sample_config(cfg: dict, max_envs: int) -> dict:
+    c = json.loads(json.dumps(cfg))
+    c["batch"]["num_envs"] = min(int(c["batch"]["num_envs"]), max_envs)
+    return c
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    cfg, n_thr = build_config(args.config, 0, "fp32")
+    sample = cpu_sample_config(cfg, 16384)
+    n = sample["batch"]["num_envs"]
+    # warmup steps untimed, then K steps each a bounded slice of the workload
+    from oracle import oracle as orc
+    b = orc.OracleBatch(sample, threads=threads)
+    act = orc.bench_actions(0, n, b.action_dim)
+    for _ in range(args.warmup):
+        b.step(act)
+    t0 = time.perf_counter()
+    k = 0
+    budget = 120.0
+    while k < args.steps and time.perf_counter() - t0 < budget:
+        b.step(act)
+        k += 1
+    wall = time.perf_counter() - t0
+    value = n * k / wall
+    c = CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": "env_steps_per_sec", "value": value,
+        "unit": "env-steps/s", "n_gpus": args.gpus, "steps": k, "warmup": args.warmup,
+        "ms_per_step": wall / k * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["workload"], "num_envs_sampled": n,
+                   "rtf_aggregate": value * CONTROL_DT},
+        "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{n} envs x {k} steps of {args.config} on the C oracle "
+                                   f"(uuv_oracle.c, fp64, OpenMP {threads} threads); the Rust "
+                                   "reference engine cannot be built (no cargo/rustc)"},
+        "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-sweep", action="store_true", help="skip the secondary config sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_14117_b200 as uuv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dev = rank_device()
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg, n_thr = build_config(args.config, rank, args.precision)
+    c = CONFIGS[args.config]
+    env = uuv.B200EnvBatch(cfg)
+    n = env.num_envs
+    stream = torch.cuda.current_stream()
+    act = env.bench_actions_tensor()
+    env.capture_graph(act, n_steps=1)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        env.replay_graph()
+    env.stats(clear=True)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed between steps, events per step
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            env.replay_graph()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        # episode statistics: one NCCL all-reduce per timed window (not per step)
+        st = env.stats_tensor(clear=False)
+        if world > 1:
+            dist.all_reduce(st)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    local_s = sum(step_ms) / 1e3
+    elapsed = max_over_ranks(local_s)
+    value = n * world * args.steps / elapsed
+    ms_per_step = elapsed / args.steps * 1e3
+    clocks = clk.summary()
+    stats = dict(zip(uuv.STAT_NAMES, st.double().cpu().tolist()))
+
+    # ---- steady-state (L2-resident, back-to-back graph replays) for reference
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        env.replay_graph()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    b2b_ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- e2e through the reference-facing C ABI with pinned host f64 buffers
+    act_h = torch.empty((n, env.action_dim), dtype=torch.float64, pin_memory=True)
+    act_h.copy_(act.double().cpu())
+    act_np = act_h.numpy()
+    env.use_pinned_host_buffers()
+    for _ in range(args.warmup):
+        env.step(act_np)
+    barrier()
+    k_e2e = max(10, min(args.steps, 300))
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        obs, rew, done = env.step(act_np)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = n * world * k_e2e / e2e_s
+    h2d = n * env.action_dim * 8
+    d2h = n * env.obs_dim * 8 + n * 8 + n * 1
+
+    # ---- roofline of the step kernel (FP32 pipe bound)
+    hbm_peak, sm_max_mhz, peak_src = measured_peaks()
+    sm_count = int(env.info["sm_count"])
+    clk_mhz = sm_max_mhz
+    fp32_peak = sm_count * 128 * 2 * clk_mhz * 1e6 / 1e12   # TFLOP/s
+    fl = flops_per_env_step(c["kind"], n_thr)
+    kern_s = local_s / args.steps
+    achieved = fl * n / kern_s / 1e12
+    bpe = bytes_per_env_step(c["kind"], env.action_dim, env.obs_dim, bool(c["dr"]))
+    hbm_achieved = bpe * n / kern_s / 1e9
+
+    line = {
+        "metric": "env_steps_per_sec", "value": value, "unit": "env-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
+        "config": {"workload": c["workload"], "num_envs_per_gpu": n, "num_envs_total": n * world,
+                   "task": c["kind"], "vehicles": c["vehicles"],
+                   "randomization": c["dr"] or "none", "n_substeps": 10,
+                   "control_dt": CONTROL_DT, "parallelism": f"env-slab x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "step": "1 fused kernel per step, CUDA-graph replay"},
+        "rtf": {"aggregate": value * CONTROL_DT,
+                "per_env": CONTROL_DT / (ms_per_step / 1e3),
+                "per_env_l2_resident": CONTROL_DT / (b2b_ms / 1e3)},
+        "steady_state": {"ms_per_step": b2b_ms, "value": n * world / (b2b_ms / 1e3),
+                         "note": "back-to-back graph replays, L2 not flushed"},
+        "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": k_e2e,
+                "path": "uuvsim_step C ABI v1, pinned host f64 buffers"},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak,
+                     "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                     "traffic": profile_traffic(args.config),
+                     "flops_per_env_step": fl,
+                     "peak_source": f"derived: {sm_count} SMs x 128 FP32 lanes x 2 x "
+                                    f"{clk_mhz:.0f} MHz (sm_max_mhz, {peak_src})",
+                     "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": hbm_achieved / hbm_peak, "bytes_per_env_step": bpe,
+                             "peak_source": peak_src}},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "episode_stats": stats,
+        "engine": {k: env.info[k] for k in ("precision", "block", "grid", "step_kernel_registers",
+                                            "device_name", "sm_count")},
+    }
+
+    # ---- secondary sizes (parity-test configs as bench lines are not allowed; these
+    # are reported inside the one JSON line for the roofline at scale)
+    if not args.no_sweep and world == 1:
+        sweep = []
+        del env
+        torch.cuda.empty_cache()
+        for name in ("c4", "c3", "c5"):
+            if name == args.config:
+                continue
+            cfg2, nt2 = build_config(name, rank, args.precision)
+            e2 = uuv.B200EnvBatch(cfg2)
+            a2 = e2.bench_actions_tensor()
+            e2.capture_graph(a2, n_steps=1)
+            for _ in range(5):
+                e2.replay_graph()
+            torch.cuda.synchronize()
+            k2 = 50
+            times = []
+            for _ in range(k2):
+                flush.zero_()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                e2.replay_graph()
+                s1.record(stream)
+                times.append((s0, s1))
+            torch.cuda.synchronize()
+            ks = sum(a.elapsed_time(b) for a, b in times) / 1e3 / k2
+            c2 = CONFIGS[name]
+            fl2 = flops_per_env_step(c2["kind"], nt2)
+            b2 = bytes_per_env_step(c2["kind"], e2.action_dim, e2.obs_dim, bool(c2["dr"]))
+            sweep.append({"config": name, "workload": c2["workload"],
+                          "num_envs": e2.num_envs, "ms_per_step": ks * 1e3,
+                          "env_steps_per_sec": e2.num_envs / ks,
+                          "fp32_frac": fl2 * e2.num_envs / ks / 1e12 / fp32_peak,
+                          "hbm_frac": b2 * e2.num_envs / ks / 1e9 / hbm_peak,
+                          "registers": e2.info["step_kernel_registers"]})
+            del e2, a2
+            torch.cuda.empty_cache()
+        line["sweep"] = sweep
+
+    # ---- CPU baseline: the oracle port on this box's host cores (rank 0, N=1)
+    if not args.no_cpu and world == 1 and rank == 0:
+        threads = os.cpu_count() or 1
+        sample = cpu_sample_config(cfg, 16384)
+        v, k, wall = cpu_oracle_run(sample, 100000, 10.0, threads)
+        line["cpu_baseline"] = {
+            "value": v, "unit": "env-steps/s", "cores": threads, "kind": "port",
+            "sample": f"{sample['batch']['num_envs']} envs x {k} steps ({wall:.1f} s) of "
+                      f"{args.config} on the C oracle (fp64, OpenMP {threads} threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

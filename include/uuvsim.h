@@ -1,0 +1,116 @@
+/*
+ * uuvsim.h -- C ABI of the B200 env-step engine (libuuvsim_core.so).
+ *
+ * Part 1 is a drop-in for the reference's ABI v1 (reference
+ * pkg/native/src/capi.rs): same ten symbols, same argument meaning, same
+ * error codes and thread-local last-error contract, so the reference's own
+ * ctypes binding (reference pkg/src/uuvsim/_native.py:49-78, selected with
+ * UUVSIM_CORE_LIB) drives this library unchanged.  Buffers are
+ * caller-allocated host memory, lengths are element counts, row-major,
+ * env-major; floats are f64 and done flags u8 0/1.
+ *
+ * Part 2 is the B200 device face: the same engine driven with device
+ * pointers on a caller-supplied CUDA stream (zero-copy for PyTorch tensors,
+ * CUDA-graph capturable), plus inspection/teacher-forcing entry points the
+ * parity tests use.  All signatures are plain C (no torch types).
+ *
+ * Return codes: 0 ok, 1 invalid config, 2 invalid handle, 3 bad buffer size,
+ * 4 runtime error (capi.rs:21-25).  No C++ exception ever crosses the ABI.
+ */
+#ifndef UUVSIM_H
+#define UUVSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UUVSIM_ABI_VERSION 1
+
+#define UUVSIM_OK 0
+#define UUVSIM_ERR_CONFIG 1
+#define UUVSIM_ERR_HANDLE 2
+#define UUVSIM_ERR_SIZE 3
+#define UUVSIM_ERR_RUNTIME 4
+
+/* ---------------- Part 1: reference ABI v1 (capi.rs:72-253) ---------------- */
+
+/* capi.rs:73-75 -- returns 1 */
+uint32_t uuvsim_abi_version(void);
+
+/* capi.rs:79-98 -- create an engine from a UTF-8 JSON config (engine.rs:17-94
+ * schema; extra keys: "vehicles", batch.vehicle_mix, batch.env_offset,
+ * "device": {"precision": "fp32"|"fp64", "index": n, "stats": bool}) */
+int32_t uuvsim_create(const char* config_json, uint64_t* out_handle);
+
+/* capi.rs:102-120 -- out[4] = {num_envs, obs_dim, action_dim, episode_len} */
+int32_t uuvsim_spec(uint64_t handle, uint64_t* out);
+
+/* capi.rs:123-140 -- reset all envs with a new root seed; obs_len = M*obs_dim */
+int32_t uuvsim_reset(uint64_t handle, uint64_t seed, double* obs, uint64_t obs_len);
+
+/* capi.rs:143-174 -- one lockstep step with auto-reset */
+int32_t uuvsim_step(uint64_t handle, const double* actions, uint64_t actions_len, double* obs,
+                    uint64_t obs_len, double* rew, uint64_t rew_len, uint8_t* done,
+                    uint64_t done_len);
+
+/* capi.rs:178-193 -- raw 12-component states, len = M*12 */
+int32_t uuvsim_states(uint64_t handle, double* out, uint64_t len);
+
+/* capi.rs:196-210 -- per-env control-step counters, len = M */
+int32_t uuvsim_step_counts(uint64_t handle, int64_t* out, uint64_t len);
+
+/* capi.rs:213-227 -- advisory on the GPU engine (0 = all cores) */
+int32_t uuvsim_set_threads(uint64_t handle, uint64_t n);
+
+/* capi.rs:230-237 -- stale / double destroy -> 2 */
+int32_t uuvsim_destroy(uint64_t handle);
+
+/* capi.rs:241-253 -- copies min(len, cap) bytes (not NUL-terminated), returns full length */
+int64_t uuvsim_last_error(char* buf, uint64_t cap);
+
+/* ---------------- Part 2: B200 extensions ---------------- */
+
+/* uuvsim_step plus the termination reason per env (-1 none, 0 truncation,
+ * 1 divergence, 2 failure; reference tasks.py:41-42,205) */
+int32_t uuvsim_step_ex(uint64_t handle, const double* actions, uint64_t actions_len,
+                       double* obs, uint64_t obs_len, double* rew, uint64_t rew_len,
+                       uint8_t* done, uint64_t done_len, int8_t* reason, uint64_t reason_len);
+
+/* teacher forcing / checkpoint-resume of the env slab */
+int32_t uuvsim_set_states(uint64_t handle, const double* in, uint64_t len);
+int32_t uuvsim_set_step_counts(uint64_t handle, const int64_t* in, uint64_t len);
+/* RNG counters (engine.rs:338-339, private in the reference) */
+int32_t uuvsim_counters(uint64_t handle, uint64_t* reset_ctr, uint64_t* param_ctr,
+                        uint64_t len);
+/* per-env randomised parameter record [M][10]:
+ * f_mass f_added f_dlin f_dquad f_thrust rb_x rb_y rb_z weight buoyancy */
+int32_t uuvsim_dr_factors(uint64_t handle, double* out, uint64_t len);
+/* episode statistics [8]: sum reward, dones by reason (trunc, div, fail),
+ * sum of completed-episode returns, sum of their lengths, env-steps,
+ * rejected per-episode resamples.  clear != 0 zeroes the accumulators. */
+int32_t uuvsim_stats(uint64_t handle, double* out, uint64_t len, int32_t clear);
+/* JSON description of the engine (precision, grid, registers, device) */
+int64_t uuvsim_info(uint64_t handle, char* buf, uint64_t cap);
+
+/* device face: all pointers are device memory; stream = cudaStream_t (0 = legacy) */
+int32_t uuvsim_dev_step(uint64_t handle, const float* actions, uint64_t actions_len, float* obs,
+                        uint64_t obs_len, float* rew, uint64_t rew_len, uint8_t* done,
+                        uint64_t done_len, int8_t* reason, uint64_t reason_len, uint64_t stream);
+int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, float* obs, uint64_t obs_len,
+                         uint64_t stream);
+int32_t uuvsim_dev_observe(uint64_t handle, float* obs, uint64_t obs_len, uint64_t stream);
+int32_t uuvsim_dev_bench_actions(uint64_t handle, float* actions, uint64_t len, uint64_t stream);
+int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,
+                         uint64_t stream);
+/* capture n_steps consecutive device steps on fixed buffers into a CUDA graph */
+int32_t uuvsim_dev_graph_capture(uint64_t handle, const float* actions, float* obs, float* rew,
+                                 uint8_t* done, int8_t* reason, uint32_t n_steps);
+int32_t uuvsim_dev_graph_launch(uint64_t handle, uint64_t stream);
+int32_t uuvsim_synchronize(uint64_t handle);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

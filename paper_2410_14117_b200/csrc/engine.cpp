@@ -1,0 +1,743 @@
+// engine.cpp -- host side of the B200 engine (config, validation, device slab,
+// launches).  See engine.h for the reference mapping.
+#include "engine.h"
+
+#include <array>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <thread>
+
+#include <nlohmann/json.hpp>
+
+namespace uuv {
+
+using json = nlohmann::json;
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw RuntimeError(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                           cudaGetErrorString(e) + ")");
+}
+
+// ------------------------------------------------------------------ JSON helpers
+namespace {
+
+const json* opt(const json& o, const char* k) {
+    if (!o.is_object()) return nullptr;
+    auto it = o.find(k);
+    if (it == o.end() || it->is_null()) return nullptr;
+    return &*it;
+}
+
+const json& req(const json& o, const char* k, const char* ctx) {
+    const json* v = opt(o, k);
+    if (!v) throw ConfigError(std::string("config is not valid JSON: missing field `") + k +
+                              "` in " + ctx);
+    return *v;
+}
+
+double num(const json& v, const char* name) {
+    if (!v.is_number())
+        throw ConfigError(std::string("config is not valid JSON: field `") + name +
+                          "` must be a number");
+    return v.get<double>();
+}
+
+uint64_t unum(const json& v, const char* name) {
+    if (!v.is_number_unsigned())
+        throw ConfigError(std::string("config is not valid JSON: field `") + name +
+                          "` must be a non-negative integer");
+    return v.get<uint64_t>();
+}
+
+int64_t inum(const json& v, const char* name) {
+    if (!v.is_number_integer())
+        throw ConfigError(std::string("config is not valid JSON: field `") + name +
+                          "` must be an integer");
+    return v.get<int64_t>();
+}
+
+template <size_t N>
+void fixed(const json& v, const char* name, double* out) {
+    if (!v.is_array() || v.size() != N)
+        throw ConfigError(std::string("config is not valid JSON: field `") + name +
+                          "` must be an array of " + std::to_string(N) + " numbers");
+    for (size_t i = 0; i < N; ++i) out[i] = num(v[i], name);
+}
+
+// engine.rs:160-172
+void square(const json& v, size_t side, const char* name, double* out) {
+    if (!v.is_array())
+        throw ConfigError(std::string("config is not valid JSON: field `") + name +
+                          "` must be a nested array");
+    if (v.size() != side)
+        throw ConfigError(std::string(name) + " must be " + std::to_string(side) + "x" +
+                          std::to_string(side));
+    for (size_t i = 0; i < side; ++i) {
+        if (!v[i].is_array() || v[i].size() != side)
+            throw ConfigError(std::string(name) + " must be " + std::to_string(side) + "x" +
+                              std::to_string(side));
+        for (size_t j = 0; j < side; ++j) out[i * side + j] = num(v[i][j], name);
+    }
+}
+
+// engine.rs:174-229 (BaseVehicle::from_doc)
+BaseVehicle vehicle_from_doc(const json& d) {
+    if (!d.is_object()) throw ConfigError("config is not valid JSON: vehicle must be an object");
+    BaseVehicle b;
+    b.mass = num(req(d, "mass", "vehicle"), "mass");
+    const json& inertia = req(d, "inertia", "vehicle");
+    fixed<3>(req(d, "r_g", "vehicle"), "r_g", b.rg);
+    fixed<3>(req(d, "r_b", "vehicle"), "r_b", b.rb);
+    b.weight = num(req(d, "weight", "vehicle"), "weight");
+    b.buoyancy = num(req(d, "buoyancy", "vehicle"), "buoyancy");
+    const json& added = req(d, "added_mass", "vehicle");
+    const json& dlin = req(d, "damping_linear", "vehicle");
+    fixed<6>(req(d, "damping_quadratic", "vehicle"), "damping_quadratic", b.dquad);
+    const json& th = req(d, "thrusters", "vehicle");
+    if (!th.is_array()) throw ConfigError("config is not valid JSON: thrusters must be a list");
+    if (!(b.mass > 0.0)) throw ConfigError("mass must be positive");
+    if (b.weight < 0.0 || b.buoyancy < 0.0) throw ConfigError("weight and buoyancy must be >= 0");
+    if (th.empty()) throw ConfigError("layout needs at least one thruster");
+    for (const json& t : th) {
+        std::array<double, 3> p{}, dd{};
+        fixed<3>(req(t, "position", "thruster"), "position", p.data());
+        fixed<3>(req(t, "direction", "thruster"), "direction", dd.data());
+        double kmax = num(req(t, "max_thrust", "thruster"), "max_thrust");
+        double n = std::sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]);
+        if (std::fabs(n - 1.0) > 1e-9) throw ConfigError("thruster direction must be unit norm");
+        if (!(kmax > 0.0)) throw ConfigError("max_thrust must be positive");
+        int code = 1;
+        if (const json* c = opt(t, "curve")) {
+            if (!c->is_string()) throw ConfigError("config is not valid JSON: curve must be a string");
+            std::string s = c->get<std::string>();
+            if (s == "quadratic_signed") code = 1;
+            else if (s == "linear") code = 0;
+            else throw ConfigError("unknown thrust curve \"" + s + "\"");
+        }
+        b.pos.push_back(p);
+        b.dir.push_back(dd);
+        b.kmax.push_back(kmax);
+        b.curve.push_back(code);
+    }
+    for (double q : b.dquad)
+        if (q < 0.0) throw ConfigError("damping_quadratic components must be >= 0");
+    square(inertia, 3, "inertia", b.inertia);
+    square(added, 6, "added_mass", b.added);
+    square(dlin, 6, "damping_linear", b.dlin);
+    if (b.kmax.size() > (size_t)MAX_THR)
+        throw ConfigError("at most " + std::to_string(MAX_THR) + " thrusters are supported");
+    return b;
+}
+
+// M_RB and M_total exactly as engine.rs:234-257 / vehicle.py:64-105
+void mass_matrices(const BaseVehicle& v, double* m_rb, double* m_total) {
+    const double* rg = v.rg;
+    const double s[9] = {0.0, -rg[2], rg[1], rg[2], 0.0, -rg[0], -rg[1], rg[0], 0.0};
+    const double nm = -v.mass;
+    for (int k = 0; k < 36; ++k) m_rb[k] = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        m_rb[i * 6 + i] = v.mass;
+        for (int j = 0; j < 3; ++j) {
+            m_rb[i * 6 + (j + 3)] = nm * s[i * 3 + j];
+            m_rb[(i + 3) * 6 + j] = v.mass * s[i * 3 + j];
+            m_rb[(i + 3) * 6 + (j + 3)] = v.inertia[i * 3 + j];
+        }
+    }
+    for (int k = 0; k < 36; ++k) m_total[k] = m_rb[k] + v.added[k];
+}
+
+// model.rs:38-57
+bool cholesky6(const double* m, double* L) {
+    for (int k = 0; k < 36; ++k) L[k] = 0.0;
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = m[i * 6 + j];
+            for (int k = 0; k < j; ++k) s -= L[i * 6 + k] * L[j * 6 + k];
+            if (i == j) {
+                if (s <= 0.0) return false;
+                L[i * 6 + i] = std::sqrt(s);
+            } else {
+                L[i * 6 + j] = s / L[j * 6 + j];
+            }
+        }
+    return true;
+}
+
+// task.rs:46-65
+void traj(const TaskCfg& t, double time, double o[4]) {
+    double ang = t.omega * time;
+    double ca = std::cos(ang), sa = std::sin(ang);
+    if (t.kind == 1) {
+        o[0] = t.cx + t.radius * ca; o[1] = t.cy + t.radius * sa; o[2] = t.depth;
+        o[3] = std::atan2(ca, -sa);
+    } else if (t.kind == 2) {
+        o[0] = t.cx + t.radius * ca; o[1] = t.cy + t.radius * sa;
+        o[2] = t.depth + t.climb * time;
+        o[3] = std::atan2(ca, -sa);
+    } else {
+        o[0] = t.cx + t.scale * ca; o[1] = t.cy + t.scale * (sa * ca); o[2] = t.depth;
+        double c2a = ca * ca - sa * sa;
+        o[3] = std::atan2(c2a, -sa);
+    }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ parsing
+void Engine::parse(const std::string& text) {
+    json doc;
+    try {
+        doc = json::parse(text);
+    } catch (const std::exception& e) {
+        throw ConfigError(std::string("config is not valid JSON: ") + e.what());
+    }
+    if (!doc.is_object()) throw ConfigError("config is not valid JSON: expected an object");
+    seed_ = unum(req(doc, "seed", "config"), "seed");
+
+    // vehicle(s): "vehicles" (extension, mixed batches) > "vehicle" > "vehicle_params"
+    if (const json* vs = opt(doc, "vehicles")) {
+        if (!vs->is_array() || vs->empty() || vs->size() > (size_t)MAX_VEH)
+            throw ConfigError("vehicles must list 1.." + std::to_string(MAX_VEH) + " vehicle documents");
+        for (const json& v : *vs) veh_.push_back(vehicle_from_doc(v));
+    } else if (const json* v = opt(doc, "vehicle")) {
+        veh_.push_back(vehicle_from_doc(*v));
+    } else if (const json* path = opt(doc, "vehicle_params")) {
+        if (!path->is_string()) throw ConfigError("config is not valid JSON: vehicle_params must be a path");
+        std::string p = path->get<std::string>();
+        std::ifstream f(p);
+        if (!f) throw ConfigError("cannot read vehicle parameter file " + p);
+        std::stringstream ss;
+        ss << f.rdbuf();
+        json vd;
+        try {
+            vd = json::parse(ss.str());
+        } catch (const std::exception& e) {
+            throw ConfigError("vehicle parameter file " + p + ": " + e.what());
+        }
+        veh_.push_back(vehicle_from_doc(vd));
+    } else {
+        throw ConfigError("config must include 'vehicle' or 'vehicle_params'");
+    }
+
+    // task (engine.rs:363-404)
+    json t = json::object();
+    if (const json* tj = opt(doc, "task")) t = *tj;
+    if (const json* k = opt(t, "kind")) {
+        if (!k->is_string()) throw ConfigError("config is not valid JSON: task.kind must be a string");
+        std::string s = k->get<std::string>();
+        if (s == "station_keeping") task_.kind = 0;
+        else if (s == "circle") task_.kind = 1;
+        else if (s == "helix") task_.kind = 2;
+        else if (s == "lemniscate") task_.kind = 3;
+        else throw ConfigError("unknown task kind \"" + s + "\"");
+    }
+    if (const json* v = opt(t, "target")) fixed<6>(*v, "target", task_.target);
+    if (const json* v = opt(t, "center")) {
+        double c[2];
+        fixed<2>(*v, "center", c);
+        task_.cx = c[0]; task_.cy = c[1];
+    }
+    if (const json* v = opt(t, "radius")) task_.radius = num(*v, "radius");
+    if (const json* v = opt(t, "angular_rate")) task_.omega = num(*v, "angular_rate");
+    if (const json* v = opt(t, "climb_rate")) task_.climb = num(*v, "climb_rate");
+    if (const json* v = opt(t, "scale")) task_.scale = num(*v, "scale");
+    if (const json* v = opt(t, "depth")) task_.depth = num(*v, "depth");
+    if (const json* v = opt(t, "lookahead")) task_.lookahead = (int)std::min<uint64_t>(unum(*v, "lookahead"), 1u << 20);
+    if (const json* v = opt(t, "episode_len")) task_.episode_len = inum(*v, "episode_len");
+    if (const json* v = opt(t, "control_dt")) task_.control_dt = num(*v, "control_dt");
+    if (const json* v = opt(t, "n_substeps")) {
+        uint64_t n = unum(*v, "n_substeps");
+        if (n > UINT32_MAX) throw ConfigError("config is not valid JSON: n_substeps out of range");
+        task_.n_substeps = (int)std::min<uint64_t>(n, INT32_MAX);
+    }
+    if (!(task_.control_dt > 0.0) || task_.n_substeps < 1 || task_.lookahead < 1 ||
+        task_.episode_len < 1)
+        throw ConfigError("invalid task timing settings");
+    if ((task_.kind == 1 || task_.kind == 2) && !(task_.radius > 0.0))
+        throw ConfigError("radius must be positive");
+    if (task_.kind == 3 && !(task_.scale > 0.0)) throw ConfigError("scale must be positive");
+    if (task_.episode_len > (int64_t)INT32_MAX - task_.lookahead - 2)
+        throw ConfigError("episode_len too large for the device step counter (int32)");
+
+    // batch (engine.rs:406-417)
+    json b = json::object();
+    if (const json* bj = opt(doc, "batch")) b = *bj;
+    m_ = 64;
+    if (const json* v = opt(b, "num_envs")) m_ = (int64_t)unum(*v, "num_envs");
+    if (m_ < 1) throw ConfigError("batch.num_envs must be >= 1");
+    if (m_ > (int64_t)INT32_MAX - BLOCK) throw ConfigError("batch.num_envs too large for one device slab");
+    threads = 0;
+    if (const json* v = opt(b, "threads")) threads = (int)std::min<uint64_t>(unum(*v, "threads"), 1 << 16);
+    if (threads == 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    if (const json* r = opt(b, "randomization")) {   // engine.rs:108-134
+        if (!r->is_object()) throw ConfigError("config is not valid JSON: randomization must be an object");
+        ranges_.enabled = true;
+        struct { const char* name; double* dst; } rs[] = {
+            {"mass", ranges_.mass}, {"added_mass", ranges_.added},
+            {"damping_linear", ranges_.dlin}, {"damping_quadratic", ranges_.dquad},
+            {"max_thrust", ranges_.thrust}, {"buoyancy_ratio", ranges_.ratio}};
+        for (auto& x : rs)
+            if (const json* v = opt(*r, x.name)) fixed<2>(*v, x.name, x.dst);
+        if (const json* v = opt(*r, "rb_offset")) ranges_.rb_offset = num(*v, "rb_offset");
+        if (const json* v = opt(*r, "per_episode")) {
+            if (!v->is_boolean()) throw ConfigError("config is not valid JSON: per_episode must be a bool");
+            ranges_.per_episode = v->get<bool>();
+        }
+        for (auto& x : rs)
+            if (!(0.0 < x.dst[0] && x.dst[0] <= x.dst[1]))
+                throw ConfigError(std::string("range ") + x.name + " must satisfy 0 < lo <= hi");
+        if (ranges_.rb_offset < 0.0) throw ConfigError("rb_offset must be >= 0");
+    }
+    // extensions: global env offset (sharding) and contiguous vehicle mix
+    if (const json* v = opt(b, "env_offset")) env_offset_ = unum(*v, "env_offset");
+    if (const json* v = opt(b, "vehicle_mix")) {
+        if (!v->is_array() || v->size() != veh_.size())
+            throw ConfigError("batch.vehicle_mix must give one env count per vehicle");
+        for (const json& c : *v) mix_.push_back((int64_t)unum(c, "vehicle_mix"));
+    }
+    if (veh_.size() > 1 && mix_.empty())
+        throw ConfigError("several vehicles need batch.vehicle_mix");
+    // device section (extension; unknown keys are ignored like serde)
+    if (const json* d = opt(doc, "device")) {
+        if (const json* v = opt(*d, "precision")) {
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "fp32") fp64_ = false;
+            else if (s == "fp64") fp64_ = true;
+            else throw ConfigError("device.precision must be \"fp32\" or \"fp64\"");
+        }
+        if (const json* v = opt(*d, "index")) device_ = (int)inum(*v, "device.index");
+        if (const json* v = opt(*d, "stats")) {
+            if (!v->is_boolean()) throw ConfigError("device.stats must be a bool");
+            stats_on_ = v->get<bool>();
+        }
+    } else {
+        cudaGetDevice(&device_);
+    }
+
+    obs_dim_ = task_.kind == 0 ? 12 : 6 * task_.lookahead + 6;
+    n_act_ = 0;
+    for (auto& v : veh_) n_act_ = std::max<int>(n_act_, (int)v.kmax.size());
+}
+
+template <> EngineP<float>& Engine::P<float>() { return *pf_; }
+template <> EngineP<double>& Engine::P<double>() { return *pd_; }
+
+template <class T> void Engine::fill_params(EngineP<T>& p) {
+    std::memset(&p, 0, sizeof(p));
+    for (size_t vi = 0; vi < veh_.size(); ++vi) {
+        const BaseVehicle& v = veh_[vi];
+        VehP<T>& V = p.veh[vi];
+        double m_rb[36], m_total[36], L[36];
+        mass_matrices(v, m_rb, m_total);
+        if (!cholesky6(m_total, L))
+            throw ConfigError("M_RB + M_A is not positive definite: matrix is not positive definite");
+        for (int k = 0; k < 36; ++k) {
+            V.mtot[k] = (T)m_total[k];
+            V.mrb[k] = (T)m_rb[k];
+            V.ma[k] = (T)v.added[k];
+            V.chol[k] = (T)L[k];
+            V.dlin[k] = (T)v.dlin[k];
+            V.mrb64[k] = m_rb[k];
+            V.ma64[k] = v.added[k];
+        }
+        for (int i = 0; i < 6; ++i) {
+            V.chol_inv[i] = (T)(1.0 / L[i * 6 + i]);
+            V.dquad[i] = (T)v.dquad[i];
+        }
+        V.weight = (T)v.weight;
+        V.buoyancy = (T)v.buoyancy;
+        for (int k = 0; k < 3; ++k) {
+            V.rg[k] = (T)v.rg[k];
+            V.rb[k] = (T)v.rb[k];
+            V.rb64[k] = v.rb[k];
+        }
+        V.weight64 = v.weight;
+        const int n = (int)v.kmax.size();
+        V.n_thr = n;
+        for (int i = 0; i < n; ++i) {   // thrusters.py:81-94 / engine.rs:260-271
+            const double px = v.pos[i][0], py = v.pos[i][1], pz = v.pos[i][2];
+            const double dx = v.dir[i][0], dy = v.dir[i][1], dz = v.dir[i][2];
+            V.alloc[0 * MAX_THR + i] = (T)dx;
+            V.alloc[1 * MAX_THR + i] = (T)dy;
+            V.alloc[2 * MAX_THR + i] = (T)dz;
+            V.alloc[3 * MAX_THR + i] = (T)(py * dz - pz * dy);
+            V.alloc[4 * MAX_THR + i] = (T)(pz * dx - px * dz);
+            V.alloc[5 * MAX_THR + i] = (T)(px * dy - py * dx);
+            V.kmax[i] = (T)v.kmax[i];
+            V.curve[i] = v.curve[i];
+        }
+    }
+    TaskP<T>& tk = p.task;
+    for (int k = 0; k < 6; ++k) tk.target[k] = (T)task_.target[k];
+    tk.sub_dt = (T)(task_.control_dt / (double)task_.n_substeps);
+    tk.div_radius = (T)10.0;   // tasks.py:39
+    tk.kind = task_.kind;
+    tk.lookahead = task_.lookahead;
+    tk.n_substeps = task_.n_substeps;
+    tk.episode_len = (int32_t)task_.episode_len;
+    tk.obs_dim = obs_dim_;
+    if (task_.kind == 0) {
+        tk.spawn[0] = task_.target[0]; tk.spawn[1] = task_.target[1]; tk.spawn[2] = task_.target[2];
+        tk.ref_psi = task_.target[5];
+    } else {
+        double r[4];
+        traj(task_, 0.0, r);
+        tk.spawn[0] = r[0]; tk.spawn[1] = r[1]; tk.spawn[2] = r[2];
+        tk.ref_psi = r[3];
+    }
+    tk.traj = reinterpret_cast<const V4<T>*>(traj_);
+    RangesP& R = p.ranges;
+    R.enabled = ranges_.enabled;
+    R.per_episode = ranges_.per_episode;
+    const double* lo_hi[5] = {ranges_.mass, ranges_.added, ranges_.dlin, ranges_.dquad, ranges_.thrust};
+    for (int i = 0; i < 5; ++i) {
+        R.log_lo[i] = std::log(lo_hi[i][0]);
+        R.log_hi[i] = std::log(lo_hi[i][1]);
+    }
+    R.rb_offset = ranges_.rb_offset;
+    R.ratio[0] = ranges_.ratio[0];
+    R.ratio[1] = ranges_.ratio[1];
+    p.seed = seed_;
+    p.env_offset = env_offset_;
+    p.mix_bound0 = mix_.empty() ? INT64_MAX : mix_[0];
+    p.n_env = (int32_t)m_;
+    p.n_veh = (int32_t)veh_.size();
+    p.act_dim = n_act_;
+    p.stats_on = stats_on_ ? 1 : 0;
+    p.stats = stats_part_;
+
+    // device buffers carved from the arena
+    char* a = static_cast<char*>(arena_);
+    size_t off = 0;
+    auto carve = [&](size_t bytes) { void* q = a + off; off += align256(bytes); return q; };
+    const size_t N = (size_t)m_;
+    p.s0 = (V4<T>*)carve(N * sizeof(V4<T>));
+    p.s1 = (V4<T>*)carve(N * sizeof(V4<T>));
+    p.s2 = (V4<T>*)carve(N * sizeof(V4<T>));
+    p.step = (int32_t*)carve(N * 4);
+    p.ep_ret = (float*)carve(N * 4);
+    p.reset_ctr = (uint64_t*)carve(N * 8);
+    p.param_ctr = (uint64_t*)carve(N * 8);
+    p.seed_dev = (uint64_t*)carve(8);
+    if (ranges_.enabled) {
+        p.dr0 = (V4<T>*)carve(N * sizeof(V4<T>));
+        p.dr1 = (V4<T>*)carve(N * sizeof(V4<T>));
+        p.dr2 = (V2<T>*)carve(N * sizeof(V2<T>));
+    }
+    if (off > arena_bytes_) throw RuntimeError("internal: arena too small");
+}
+
+void Engine::activate() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
+
+void Engine::allocate() {
+    activate();
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+    device_name_ = prop.name;
+    sm_count_ = prop.multiProcessorCount;
+    const size_t N = (size_t)m_;
+    const size_t sT = fp64_ ? 8 : 4;
+    size_t bytes = 3 * align256(N * 4 * sT) + 2 * align256(N * 4) + 2 * align256(N * 8) + 256;
+    if (ranges_.enabled) bytes += 2 * align256(N * 4 * sT) + align256(N * 2 * sT);
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const size_t abi = align256(N * n_act_ * 8) + align256(N * obs_dim_ * 8) + align256(N * 8) +
+                       2 * align256(N) + align256(N * 12 * 8);
+    if (bytes + abi > free_b)
+        throw ConfigError("batch.num_envs needs " + std::to_string((bytes + abi) >> 20) +
+                          " MiB of device memory, " + std::to_string(free_b >> 20) + " MiB free");
+    arena_bytes_ = bytes;
+    cuda_check(cudaMalloc(&arena_, bytes), "cudaMalloc(state)");
+    cuda_check(cudaMemset(arena_, 0, bytes), "cudaMemset(state)");
+    nblk_ = (int)((m_ + BLOCK - 1) / BLOCK);
+    cuda_check(cudaMalloc(&stats_part_, (size_t)nblk_ * NSTAT * sizeof(double)), "cudaMalloc(stats)");
+    cuda_check(cudaMemset(stats_part_, 0, (size_t)nblk_ * NSTAT * sizeof(double)), "cudaMemset(stats)");
+    cuda_check(cudaMalloc(&d_stats_out_, NSTAT * sizeof(double)), "cudaMalloc(stats_out)");
+    if (task_.kind != 0) {   // reference trajectory by step index (task.rs:67-74)
+        const int64_t len = task_.episode_len + task_.lookahead + 1;
+        std::vector<double> tab((size_t)len * 4);
+        for (int64_t i = 0; i < len; ++i) traj(task_, (double)i * task_.control_dt, &tab[(size_t)i * 4]);
+        if (fp64_) {
+            cuda_check(cudaMalloc(&traj_, tab.size() * 8), "cudaMalloc(traj)");
+            cuda_check(cudaMemcpy(traj_, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), "traj");
+        } else {
+            std::vector<float> tf(tab.begin(), tab.end());
+            cuda_check(cudaMalloc(&traj_, tf.size() * 4), "cudaMalloc(traj)");
+            cuda_check(cudaMemcpy(traj_, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice), "traj");
+        }
+    }
+    cuda_check(cudaMalloc(&d_act64_, N * n_act_ * 8), "cudaMalloc(abi act)");
+    cuda_check(cudaMalloc(&d_obs64_, N * obs_dim_ * 8), "cudaMalloc(abi obs)");
+    cuda_check(cudaMalloc(&d_rew64_, N * 8), "cudaMalloc(abi rew)");
+    cuda_check(cudaMalloc(&d_done_, N), "cudaMalloc(abi done)");
+    cuda_check(cudaMalloc(&d_reason_, N), "cudaMalloc(abi reason)");
+    cuda_check(cudaMalloc(&d_pack_, N * 12 * 8), "cudaMalloc(abi pack)");
+    cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "cudaMalloc(flag)");
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+Engine::Engine(const std::string& text) {
+    parse(text);
+    try {
+        allocate();
+        if (fp64_) {
+            pd_ = std::make_unique<EngineP<double>>();
+            fill_params(*pd_);
+        } else {
+            pf_ = std::make_unique<EngineP<float>>();
+            fill_params(*pf_);
+        }
+        init_randomization();
+        reset_host(seed_, nullptr);
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
+Engine::~Engine() { release(); }
+
+void Engine::release() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    void* bufs[] = {arena_, traj_, stats_part_, d_act64_, d_obs64_, d_rew64_, d_done_,
+                    d_reason_, d_pack_, d_flag_, d_stats_out_};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    arena_ = traj_ = nullptr;
+    stats_part_ = d_act64_ = d_obs64_ = d_rew64_ = d_pack_ = d_stats_out_ = nullptr;
+    d_done_ = nullptr;
+    d_reason_ = nullptr;
+    d_flag_ = nullptr;
+    if (stream_) cudaStreamDestroy(stream_);
+    stream_ = nullptr;
+}
+
+void Engine::init_randomization() {   // engine.rs:440-458: per-env sample at create
+    if (!ranges_.enabled) return;
+    const int big = INT_MAX;
+    cuda_check(cudaMemcpyAsync(d_flag_, &big, sizeof(int), cudaMemcpyHostToDevice, stream_), "flag");
+    if (fp64_) cuda_check(Launch<double>::dr_init(*pd_, d_flag_, stream_), "dr_init");
+    else cuda_check(Launch<float>::dr_init(*pf_, d_flag_, stream_), "dr_init");
+    int bad = INT_MAX;
+    cuda_check(cudaMemcpyAsync(&bad, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "flag");
+    cuda_check(cudaStreamSynchronize(stream_), "dr_init sync");
+    if (bad != INT_MAX)
+        throw ConfigError("env " + std::to_string(bad) +
+                          ": randomized parameters invalid: M_RB + M_A is not positive definite: "
+                          "matrix is not positive definite");
+}
+
+// ------------------------------------------------------------------ host ABI face
+void Engine::reset_host(uint64_t seed, double* obs) {
+    activate();
+    if (fp64_) {
+        pd_->seed = seed;
+        cuda_check(Launch<double>::reset<double>(*pd_, obs ? d_obs64_ : nullptr, stream_), "reset");
+    } else {
+        pf_->seed = seed;
+        cuda_check(Launch<float>::reset<double>(*pf_, obs ? d_obs64_ : nullptr, stream_), "reset");
+    }
+    if (obs)
+        cuda_check(cudaMemcpyAsync(obs, d_obs64_, (size_t)m_ * obs_dim_ * 8, cudaMemcpyDeviceToHost,
+                                   stream_), "reset D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "reset sync");
+}
+
+void Engine::step_host(const double* act, double* obs, double* rew, uint8_t* done,
+                       int8_t* reason) {
+    activate();
+    const size_t N = (size_t)m_;
+    cuda_check(cudaMemcpyAsync(d_act64_, act, N * n_act_ * 8, cudaMemcpyHostToDevice, stream_),
+               "step H2D");
+    const bool track = task_.kind != 0, dr = ranges_.enabled;
+    if (fp64_)
+        cuda_check(Launch<double>::step<double>(*pd_, track, dr, d_act64_, d_obs64_, d_rew64_,
+                                                d_done_, d_reason_, stream_), "step");
+    else
+        cuda_check(Launch<float>::step<double>(*pf_, track, dr, d_act64_, d_obs64_, d_rew64_,
+                                               d_done_, d_reason_, stream_), "step");
+    cuda_check(cudaMemcpyAsync(obs, d_obs64_, N * obs_dim_ * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
+    cuda_check(cudaMemcpyAsync(rew, d_rew64_, N * 8, cudaMemcpyDeviceToHost, stream_), "rew D2H");
+    cuda_check(cudaMemcpyAsync(done, d_done_, N, cudaMemcpyDeviceToHost, stream_), "done D2H");
+    if (reason)
+        cuda_check(cudaMemcpyAsync(reason, d_reason_, N, cudaMemcpyDeviceToHost, stream_), "reason D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "step sync");
+}
+
+void Engine::states_host(double* out) {
+    activate();
+    if (fp64_) cuda_check(Launch<double>::pack_states(*pd_, d_pack_, stream_), "pack");
+    else cuda_check(Launch<float>::pack_states(*pf_, d_pack_, stream_), "pack");
+    cuda_check(cudaMemcpyAsync(out, d_pack_, (size_t)m_ * 12 * 8, cudaMemcpyDeviceToHost, stream_), "states D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "states sync");
+}
+
+void Engine::set_states_host(const double* in) {
+    activate();
+    cuda_check(cudaMemcpyAsync(d_pack_, in, (size_t)m_ * 12 * 8, cudaMemcpyHostToDevice, stream_), "states H2D");
+    if (fp64_) cuda_check(Launch<double>::unpack_states(*pd_, d_pack_, stream_), "unpack");
+    else cuda_check(Launch<float>::unpack_states(*pf_, d_pack_, stream_), "unpack");
+    cuda_check(cudaStreamSynchronize(stream_), "set_states sync");
+}
+
+void Engine::step_counts_host(int64_t* out) {
+    activate();
+    std::vector<int32_t> tmp((size_t)m_);
+    int32_t* src = fp64_ ? pd_->step : pf_->step;
+    cuda_check(cudaMemcpyAsync(tmp.data(), src, (size_t)m_ * 4, cudaMemcpyDeviceToHost, stream_), "steps D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "steps sync");
+    for (size_t i = 0; i < tmp.size(); ++i) out[i] = tmp[i];
+}
+
+void Engine::set_step_counts_host(const int64_t* in) {
+    activate();
+    std::vector<int32_t> tmp((size_t)m_);
+    for (size_t i = 0; i < tmp.size(); ++i) {
+        if (in[i] < 0 || in[i] >= task_.episode_len)
+            throw ConfigError("step counts must lie in [0, episode_len)");
+        tmp[i] = (int32_t)in[i];
+    }
+    int32_t* dst = fp64_ ? pd_->step : pf_->step;
+    cuda_check(cudaMemcpyAsync(dst, tmp.data(), (size_t)m_ * 4, cudaMemcpyHostToDevice, stream_), "steps H2D");
+    cuda_check(cudaStreamSynchronize(stream_), "steps sync");
+}
+
+void Engine::counters_host(uint64_t* rc, uint64_t* pc) {
+    activate();
+    uint64_t* r = fp64_ ? pd_->reset_ctr : pf_->reset_ctr;
+    uint64_t* q = fp64_ ? pd_->param_ctr : pf_->param_ctr;
+    if (rc) cuda_check(cudaMemcpyAsync(rc, r, (size_t)m_ * 8, cudaMemcpyDeviceToHost, stream_), "ctr D2H");
+    if (pc) cuda_check(cudaMemcpyAsync(pc, q, (size_t)m_ * 8, cudaMemcpyDeviceToHost, stream_), "ctr D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "ctr sync");
+}
+
+void Engine::dr_factors_host(double* out) {
+    activate();
+    if (!ranges_.enabled) {
+        for (int64_t e = 0; e < m_; ++e) {
+            const BaseVehicle& v = veh_[0];
+            double* r = out + e * 10;
+            r[0] = r[1] = r[2] = r[3] = r[4] = 1.0;
+            r[5] = v.rb[0]; r[6] = v.rb[1]; r[7] = v.rb[2];
+            r[8] = v.weight; r[9] = v.buoyancy;
+        }
+        return;
+    }
+    if (fp64_) cuda_check(Launch<double>::pack_dr(*pd_, d_pack_, stream_), "pack_dr");
+    else cuda_check(Launch<float>::pack_dr(*pf_, d_pack_, stream_), "pack_dr");
+    cuda_check(cudaMemcpyAsync(out, d_pack_, (size_t)m_ * 10 * 8, cudaMemcpyDeviceToHost, stream_), "dr D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "dr sync");
+}
+
+void Engine::stats_host(double* out, bool clear) {
+    activate();
+    cuda_check(launch_stats_reduce(stats_part_, nblk_, d_stats_out_, clear ? 1 : 0, stream_), "stats");
+    cuda_check(cudaMemcpyAsync(out, d_stats_out_, NSTAT * 8, cudaMemcpyDeviceToHost, stream_), "stats D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "stats sync");
+}
+
+// ------------------------------------------------------------------ device face
+void Engine::dev_step(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+                      cudaStream_t st) {
+    const bool track = task_.kind != 0, dr = ranges_.enabled;
+    if (fp64_) cuda_check(Launch<double>::step<float>(*pd_, track, dr, act, obs, rew, done, reason, st), "dev_step");
+    else cuda_check(Launch<float>::step<float>(*pf_, track, dr, act, obs, rew, done, reason, st), "dev_step");
+}
+
+void Engine::dev_reset(uint64_t seed, float* obs, cudaStream_t st) {
+    if (fp64_) {
+        pd_->seed = seed;
+        cuda_check(Launch<double>::reset<float>(*pd_, obs, st), "dev_reset");
+    } else {
+        pf_->seed = seed;
+        cuda_check(Launch<float>::reset<float>(*pf_, obs, st), "dev_reset");
+    }
+}
+
+void Engine::dev_observe(float* obs, cudaStream_t st) {
+    if (fp64_) cuda_check(Launch<double>::observe<float>(*pd_, obs, st), "dev_observe");
+    else cuda_check(Launch<float>::observe<float>(*pf_, obs, st), "dev_observe");
+}
+
+void Engine::dev_bench_actions(float* act, cudaStream_t st) {
+    const uint64_t seed = fp64_ ? pd_->seed : pf_->seed;
+    cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_, act, nullptr, st), "bench_actions");
+}
+
+void Engine::dev_stats(double* out, bool clear, cudaStream_t st) {
+    cuda_check(launch_stats_reduce(stats_part_, nblk_, out, clear ? 1 : 0, st), "dev_stats");
+}
+
+void Engine::graph_capture(const float* act, float* obs, float* rew, uint8_t* done,
+                           int8_t* reason, int n_steps) {
+    activate();
+    if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "capture pre-sync");
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+    try {
+        for (int i = 0; i < n_steps; ++i) dev_step(act, obs, rew, done, reason, stream_);
+    } catch (...) {
+        cudaStreamEndCapture(stream_, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(stream_, &g), "EndCapture");
+    cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+    cudaGraphDestroy(g);
+    cuda_check(e, "GraphInstantiate");
+}
+
+void Engine::graph_launch(cudaStream_t st) {
+    if (!graph_exec_) throw RuntimeError("no captured graph (call uuvsim_dev_graph_capture first)");
+    cuda_check(cudaGraphLaunch(graph_exec_, st), "GraphLaunch");
+}
+
+void Engine::synchronize() {
+    activate();
+    cuda_check(cudaDeviceSynchronize(), "synchronize");
+}
+
+std::string Engine::info() const {
+    cudaFuncAttributes a{};
+    const bool track = task_.kind != 0, dr = ranges_.enabled, mix = veh_.size() > 1;
+    if (fp64_) Launch<double>::step_attrs(&a, track, dr, mix);
+    else Launch<float>::step_attrs(&a, track, dr, mix);
+    json j = {
+        {"engine", "paper_2410_14117_b200"},
+        {"abi_version", 1},
+        {"precision", fp64_ ? "fp64" : "fp32"},
+        {"num_envs", m_},
+        {"env_offset", env_offset_},
+        {"obs_dim", obs_dim_},
+        {"action_dim", n_act_},
+        {"episode_len", task_.episode_len},
+        {"n_substeps", task_.n_substeps},
+        {"task_kind", task_.kind},
+        {"n_vehicles", veh_.size()},
+        {"randomization", ranges_.enabled},
+        {"per_episode", ranges_.per_episode},
+        {"device", device_},
+        {"device_name", device_name_},
+        {"sm_count", sm_count_},
+        {"block", BLOCK},
+        {"grid", nblk_},
+        {"step_kernel_registers", a.numRegs},
+        {"step_kernel_local_bytes", a.localSizeBytes},
+        {"param_block_bytes", fp64_ ? sizeof(EngineP<double>) : sizeof(EngineP<float>)},
+        {"seed", fp64_ ? pd_->seed : pf_->seed},
+    };
+    return j.dump();
+}
+
+}  // namespace uuv

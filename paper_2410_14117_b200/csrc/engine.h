@@ -1,0 +1,146 @@
+// engine.h -- host-side B200 engine: config -> device slab -> launches.
+//
+// Mirrors the reference's Engine (native/src/engine.rs:329-580): JSON config
+// parsing and validation (engine.rs:17-135, 174-229, 350-459), base-vehicle
+// kernel construction (engine.rs:234-286), per-env domain randomisation
+// (engine.rs:289-323, here the K3 kernel), reset (462-471) and the lockstep
+// step (482-580, here one K1 launch).  State lives on the GPU; host f64 buffers
+// are only touched by the C-ABI copy path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+
+namespace uuv {
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// Base vehicle, fp64 (engine.rs:141-229)
+struct BaseVehicle {
+    double mass = 0, weight = 0, buoyancy = 0;
+    double inertia[9] = {}, rg[3] = {}, rb[3] = {};
+    double added[36] = {}, dlin[36] = {}, dquad[6] = {};
+    std::vector<std::array<double, 3>> pos, dir;
+    std::vector<double> kmax;
+    std::vector<int> curve;
+};
+
+struct TaskCfg {
+    int kind = 0;
+    double target[6] = {0, 0, 2, 0, 0, 0};
+    double cx = 0, cy = 0, radius = 1, omega = 0.1, climb = 0.05, scale = 2, depth = 2;
+    int lookahead = 5;
+    int64_t episode_len = 600;
+    double control_dt = 0.05;
+    int n_substeps = 10;
+};
+
+struct RangesCfg {
+    bool enabled = false, per_episode = false;
+    double mass[2] = {1, 1}, added[2] = {1, 1}, dlin[2] = {1, 1}, dquad[2] = {1, 1},
+           thrust[2] = {1, 1}, ratio[2] = {1, 1};
+    double rb_offset = 0;
+};
+
+class Engine {
+public:
+    explicit Engine(const std::string& config_json);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // dims (uuvsim_spec)
+    int64_t num_envs() const { return m_; }
+    int obs_dim() const { return obs_dim_; }
+    int action_dim() const { return n_act_; }
+    int64_t episode_len() const { return task_.episode_len; }
+    int threads = 1;
+
+    // host-f64 ABI face (capi.rs:123-210)
+    void reset_host(uint64_t seed, double* obs);
+    void step_host(const double* act, double* obs, double* rew, uint8_t* done, int8_t* reason);
+    void states_host(double* out);
+    void step_counts_host(int64_t* out);
+    void set_states_host(const double* in);
+    void set_step_counts_host(const int64_t* in);
+    void counters_host(uint64_t* reset_ctr, uint64_t* param_ctr);
+    void dr_factors_host(double* out);     // [M][10]
+    void stats_host(double* out, bool clear);
+
+    // device face (zero-copy, stream-ordered, graph-capturable)
+    void dev_step(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+                  cudaStream_t st);
+    void dev_reset(uint64_t seed, float* obs, cudaStream_t st);
+    void dev_observe(float* obs, cudaStream_t st);
+    void dev_bench_actions(float* act, cudaStream_t st);
+    void dev_stats(double* out, bool clear, cudaStream_t st);
+    void graph_capture(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+                       int n_steps);
+    void graph_launch(cudaStream_t st);
+    void synchronize();
+    std::string info() const;
+    void activate() const;
+
+private:
+    void parse(const std::string& text);
+    void release();
+    void build_params();
+    void allocate();
+    void init_randomization();
+    template <class T> EngineP<T>& P();
+    template <class T> void fill_params(EngineP<T>& p);
+
+    // config
+    uint64_t seed_ = 0;
+    uint64_t env_offset_ = 0;
+    int64_t m_ = 0;
+    int obs_dim_ = 0, n_act_ = 0;
+    bool fp64_ = false;
+    bool stats_on_ = true;
+    int device_ = 0;
+    std::vector<BaseVehicle> veh_;
+    std::vector<int64_t> mix_;
+    TaskCfg task_;
+    RangesCfg ranges_;
+
+    // launch parameter blocks (one live, by precision)
+    std::unique_ptr<EngineP<float>> pf_;
+    std::unique_ptr<EngineP<double>> pd_;
+
+    // device memory
+    void* arena_ = nullptr;
+    size_t arena_bytes_ = 0;
+    void* traj_ = nullptr;
+    double* stats_part_ = nullptr;
+    int nblk_ = 0;
+    // ABI staging (f64 host layout)
+    double* d_act64_ = nullptr;
+    double* d_obs64_ = nullptr;
+    double* d_rew64_ = nullptr;
+    uint8_t* d_done_ = nullptr;
+    int8_t* d_reason_ = nullptr;
+    double* d_pack_ = nullptr;
+    int* d_flag_ = nullptr;
+    double* d_stats_out_ = nullptr;
+    cudaStream_t stream_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    std::string device_name_;
+    int sm_count_ = 0;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+}  // namespace uuv

@@ -1,0 +1,30 @@
+// launch.h -- host-visible launcher declarations (definitions in uuv_kernels.cuh,
+// explicitly instantiated by k_f32.cu / k_f64.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "uuv_common.cuh"
+
+namespace uuv {
+
+constexpr int BLOCK = 128;   // threads per block of the env kernels (one env per thread)
+
+template <class T> struct Launch {
+    template <class IO>
+    static cudaError_t step(const EngineP<T>& p, bool track, bool dr, const IO* act, IO* obs,
+                            IO* rew, uint8_t* done, int8_t* reason, cudaStream_t st);
+    template <class IO> static cudaError_t reset(const EngineP<T>& p, IO* obs, cudaStream_t st);
+    template <class IO> static cudaError_t observe(const EngineP<T>& p, IO* obs, cudaStream_t st);
+    static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);
+    static cudaError_t pack_states(const EngineP<T>& p, double* out, cudaStream_t st);
+    static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
+    static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
+    static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool mix);
+};
+
+cudaError_t launch_bench_actions(uint64_t seed, uint64_t env_offset, int n_env, int act_dim,
+                                 float* out_f32, double* out_f64, cudaStream_t st);
+cudaError_t launch_stats_reduce(double* part, int nblk, double* out, int clear, cudaStream_t st);
+
+}  // namespace uuv

@@ -1,0 +1,109 @@
+"""Parity report: error statistics of the B200 engine against the C oracle.
+
+    python tools/parity_report.py [--out gpurun_out/parity.json]
+
+For each config: teacher-forced single-step errors (per state component, max
+abs / max scaled-by-tolerance, counts outside tolerance with their input
+pitch), and free-rollout drift over 100 steps.  Used to derive the documented
+bounds in DESIGN.md; the pass/fail gates live in tests/test_gpu_parity.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2410_14117_b200 as uuv  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+from tests import parity as P  # noqa: E402
+from tests.test_gpu_parity import CONFIGS, _cfg  # noqa: E402
+
+
+def teacher_forced(cfg, steps=36):
+    gpu = uuv.B200EnvBatch(cfg)
+    ref = orc.OracleBatch(cfg, threads=8)
+    act = orc.bench_actions(cfg["seed"], ref.num_envs, ref.action_dim)
+    worst = np.zeros(12)
+    worst_scaled = np.zeros(12)
+    outs = []
+    n_done_mismatch = 0
+    n_band = 0
+    for t in range(steps):
+        s_in = ref.states()
+        gpu.set_states(s_in)
+        gpu.set_step_counts(ref.step_counts())
+        og, rg, dg, qg = gpu.step_ex(act)
+        orr, rr, dr, qr = ref.step(act, with_reason=True)
+        n_done_mismatch += int((dg != dr).sum())
+        sg, sr = gpu.states(), ref.states()
+        band = (np.abs(s_in[:, 4]) > P.PITCH_BAND) | (np.abs(sr[:, 4]) > P.PITCH_BAND)
+        n_band += int(band.sum())
+        live = ~dr & ~band
+        err = P.abs_err(sg[live], sr[live], P.STATE_ANGLES)
+        scaled = err / (P.ABS_TOL + P.REL_TOL * np.abs(sr[live]))
+        worst = np.maximum(worst, err.max(axis=0))
+        worst_scaled = np.maximum(worst_scaled, scaled.max(axis=0))
+        idx = np.argwhere(scaled > 1.0)
+        for e_, c_ in idx[:20]:
+            env = np.flatnonzero(live)[e_]
+            outs.append({"t": t, "env": int(env), "comp": int(c_),
+                         "theta_in": float(s_in[env, 4]), "got": float(sg[env, c_]),
+                         "want": float(sr[env, c_]), "err": float(err[e_, c_]),
+                         "in": s_in[env].tolist()})
+    gpu.close()
+    return {"max_abs_err": worst.tolist(), "max_err_over_tol": worst_scaled.tolist(),
+            "n_outside": len(outs), "outside": outs[:20], "done_mismatch": n_done_mismatch,
+            "n_band_env_steps": n_band, "env_steps": steps * ref.num_envs}
+
+
+def rollout(cfg, steps=100, scale=0.3):
+    gpu = uuv.B200EnvBatch(cfg)
+    ref = orc.OracleBatch(cfg, threads=8)
+    act = scale * orc.bench_actions(cfg["seed"], ref.num_envs, ref.action_dim)
+    ever = np.zeros(ref.num_envs, dtype=bool)
+    drift = []
+    mism = 0
+    for t in range(steps):
+        og, rg, dg = gpu.step(act)
+        orr, rr, dr = ref.step(act)
+        mism += int((dg != dr).sum())
+        sr = ref.states()
+        ever |= np.abs(sr[:, 4]) > P.PITCH_BAND
+        err = P.abs_err(gpu.states(), sr, P.STATE_ANGLES)
+        drift.append(float(err[~ever].max()) if (~ever).any() else 0.0)
+    gpu.close()
+    return {"drift_by_step": drift[::10] + [drift[-1]], "max_drift": max(drift),
+            "n_band_envs": int(ever.sum()), "done_mismatch": mism}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/parity.json")
+    ap.add_argument("--configs", default=",".join(CONFIGS))
+    args = ap.parse_args()
+    rep = {}
+    for name in args.configs.split(","):
+        cfg = _cfg(**CONFIGS[name])
+        rep[name] = {"teacher_forced": teacher_forced(cfg), "rollout_0.3": rollout(cfg)}
+        tf = rep[name]["teacher_forced"]
+        print(name, "tf max_err/tol", np.round(tf["max_err_over_tol"], 3).tolist(),
+              "outside", tf["n_outside"], "rollout drift", rep[name]["rollout_0.3"]["max_drift"],
+              flush=True)
+    for prec_name, prec in (("fp64_lemniscate", "fp64"),):
+        cfg = _cfg(kind="lemniscate", dr="episode", episode_len=37, n=2048, precision=prec)
+        rep[prec_name] = {"rollout_0.3": rollout(cfg, 150), "rollout_1.0": rollout(cfg, 150, 1.0)}
+        print(prec_name, rep[prec_name]["rollout_0.3"]["max_drift"],
+              rep[prec_name]["rollout_1.0"]["max_drift"], flush=True)
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps(rep, indent=1))
+
+
+if __name__ == "__main__":
+    main()
