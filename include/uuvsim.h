@@ -94,18 +94,20 @@ int32_t uuvsim_stats(uint64_t handle, double* out, uint64_t len, int32_t clear);
 /* JSON description of the engine (precision, grid, registers, device) */
 int64_t uuvsim_info(uint64_t handle, char* buf, uint64_t cap);
 
-/* device face: all pointers are device memory; stream = cudaStream_t (0 = legacy) */
-int32_t uuvsim_dev_step(uint64_t handle, const float* actions, uint64_t actions_len, float* obs,
-                        uint64_t obs_len, float* rew, uint64_t rew_len, uint8_t* done,
+/* device face: all pointers are device memory; stream = cudaStream_t (0 = legacy).
+ * actions/obs/rew elements are the engine precision: float for "fp32" engines
+ * (default), double for "fp64" engines (see uuvsim_info). */
+int32_t uuvsim_dev_step(uint64_t handle, const void* actions, uint64_t actions_len, void* obs,
+                        uint64_t obs_len, void* rew, uint64_t rew_len, uint8_t* done,
                         uint64_t done_len, int8_t* reason, uint64_t reason_len, uint64_t stream);
-int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, float* obs, uint64_t obs_len,
+int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, void* obs, uint64_t obs_len,
                          uint64_t stream);
-int32_t uuvsim_dev_observe(uint64_t handle, float* obs, uint64_t obs_len, uint64_t stream);
-int32_t uuvsim_dev_bench_actions(uint64_t handle, float* actions, uint64_t len, uint64_t stream);
+int32_t uuvsim_dev_observe(uint64_t handle, void* obs, uint64_t obs_len, uint64_t stream);
+int32_t uuvsim_dev_bench_actions(uint64_t handle, void* actions, uint64_t len, uint64_t stream);
 int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,
                          uint64_t stream);
 /* capture n_steps consecutive device steps on fixed buffers into a CUDA graph */
-int32_t uuvsim_dev_graph_capture(uint64_t handle, const float* actions, float* obs, float* rew,
+int32_t uuvsim_dev_graph_capture(uint64_t handle, const void* actions, void* obs, void* rew,
                                  uint8_t* done, int8_t* reason, uint32_t n_steps);
 int32_t uuvsim_dev_graph_launch(uint64_t handle, uint64_t stream);
 int32_t uuvsim_synchronize(uint64_t handle);

@@ -183,14 +183,21 @@ class B200EnvBatch:
             import torch
             dev = torch.device("cuda", self.device_index)
             n = self.num_envs
+            dt = self.dtype
             self._t = {
-                "obs": torch.zeros((n, self.obs_dim), dtype=torch.float32, device=dev),
-                "rew": torch.zeros(n, dtype=torch.float32, device=dev),
+                "obs": torch.zeros((n, self.obs_dim), dtype=dt, device=dev),
+                "rew": torch.zeros(n, dtype=dt, device=dev),
                 "done": torch.zeros(n, dtype=torch.uint8, device=dev),
                 "reason": torch.zeros(n, dtype=torch.int8, device=dev),
                 "stats": torch.zeros(8, dtype=torch.float64, device=dev),
             }
         return self._t
+
+    @property
+    def dtype(self):
+        """torch dtype of the device face: float32 (fp32 engine) or float64 (fp64)."""
+        import torch
+        return torch.float64 if self.precision == "fp64" else torch.float32
 
     @staticmethod
     def _stream(stream=None) -> int:
@@ -200,11 +207,11 @@ class B200EnvBatch:
 
     def _check_actions(self, actions):
         import torch
-        if (not isinstance(actions, torch.Tensor) or actions.dtype != torch.float32
+        if (not isinstance(actions, torch.Tensor) or actions.dtype != self.dtype
                 or not actions.is_cuda or actions.device.index != self.device_index
                 or tuple(actions.shape) != (self.num_envs, self.action_dim)
                 or not actions.is_contiguous()):
-            raise ValueError(f"actions must be a contiguous float32 CUDA tensor of shape "
+            raise ValueError(f"actions must be a contiguous {self.dtype} CUDA tensor of shape "
                              f"{(self.num_envs, self.action_dim)} on cuda:{self.device_index}")
 
     def reset_tensors(self, seed: int | None = None, stream=None):
@@ -219,7 +226,9 @@ class B200EnvBatch:
         return t["obs"]
 
     def step_tensors(self, actions, stream=None):
-        """One fused step on device tensors -> (obs, rew, done u8, reason i8) (reused)."""
+        """One fused step on device tensors -> (obs, rew, done u8, reason i8) (reused).
+
+        Element dtype is ``self.dtype`` (float32 for the default fp32 engine)."""
         self._require_open()
         self._check_actions(actions)
         t = self._tensors()
@@ -239,7 +248,7 @@ class B200EnvBatch:
     def bench_actions_tensor(self, stream=None):
         """Fixed U[-1,1] bench actions (reference batch.py:168-176) generated on device."""
         import torch
-        out = torch.empty((self.num_envs, self.action_dim), dtype=torch.float32,
+        out = torch.empty((self.num_envs, self.action_dim), dtype=self.dtype,
                           device=torch.device("cuda", self.device_index))
         _core.check(self._lib, self._lib.uuvsim_dev_bench_actions(
             self._handle, out.data_ptr(), out.numel(), self._stream(stream)))

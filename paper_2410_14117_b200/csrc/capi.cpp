@@ -237,15 +237,16 @@ int64_t uuvsim_info(uint64_t h, char* buf, uint64_t cap) {
     return copy_out(s, buf, cap);
 }
 
-int32_t uuvsim_dev_step(uint64_t h, const float* act, uint64_t act_len, float* obs,
-                        uint64_t obs_len, float* rew, uint64_t rew_len, uint8_t* done,
+int32_t uuvsim_dev_step(uint64_t h, const void* act, uint64_t act_len, void* obs,
+                        uint64_t obs_len, void* rew, uint64_t rew_len, uint8_t* done,
                         uint64_t done_len, int8_t* reason, uint64_t reason_len, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t m = (uint64_t)e.num_envs();
         const uint64_t want_act = m * e.action_dim(), want_obs = m * e.obs_dim();
-        if (!act || act_len != want_act) return bad_size("actions", want_act, "f32");
-        if (!obs || obs_len != want_obs) return bad_size("obs", want_obs, "f32");
-        if (!rew || rew_len != m) return bad_size("rewards", m, "f32");
+        const char* u = e.is_fp64() ? "f64" : "f32";
+        if (!act || act_len != want_act) return bad_size("actions", want_act, u);
+        if (!obs || obs_len != want_obs) return bad_size("obs", want_obs, u);
+        if (!rew || rew_len != m) return bad_size("rewards", m, u);
         if (!done || done_len != m) return bad_size("dones", m, "u8");
         if (reason && reason_len != m) return bad_size("reasons", m, "i8");
         e.dev_step(act, obs, rew, done, reason, as_stream(stream));
@@ -253,29 +254,29 @@ int32_t uuvsim_dev_step(uint64_t h, const float* act, uint64_t act_len, float* o
     });
 }
 
-int32_t uuvsim_dev_reset(uint64_t h, uint64_t seed, float* obs, uint64_t obs_len,
+int32_t uuvsim_dev_reset(uint64_t h, uint64_t seed, void* obs, uint64_t obs_len,
                          uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
-        if (obs && obs_len != want) return bad_size("obs", want, "f32");
+        if (obs && obs_len != want) return bad_size("obs", want, e.is_fp64() ? "f64" : "f32");
         e.dev_reset(seed, obs, as_stream(stream));
         return UUVSIM_OK;
     });
 }
 
-int32_t uuvsim_dev_observe(uint64_t h, float* obs, uint64_t obs_len, uint64_t stream) {
+int32_t uuvsim_dev_observe(uint64_t h, void* obs, uint64_t obs_len, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
-        if (!obs || obs_len != want) return bad_size("obs", want, "f32");
+        if (!obs || obs_len != want) return bad_size("obs", want, e.is_fp64() ? "f64" : "f32");
         e.dev_observe(obs, as_stream(stream));
         return UUVSIM_OK;
     });
 }
 
-int32_t uuvsim_dev_bench_actions(uint64_t h, float* act, uint64_t len, uint64_t stream) {
+int32_t uuvsim_dev_bench_actions(uint64_t h, void* act, uint64_t len, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.action_dim();
-        if (!act || len != want) return bad_size("actions", want, "f32");
+        if (!act || len != want) return bad_size("actions", want, e.is_fp64() ? "f64" : "f32");
         e.dev_bench_actions(act, as_stream(stream));
         return UUVSIM_OK;
     });
@@ -289,7 +290,7 @@ int32_t uuvsim_dev_stats(uint64_t h, double* out, uint64_t len, int32_t clear, u
     });
 }
 
-int32_t uuvsim_dev_graph_capture(uint64_t h, const float* act, float* obs, float* rew,
+int32_t uuvsim_dev_graph_capture(uint64_t h, const void* act, void* obs, void* rew,
                                  uint8_t* done, int8_t* reason, uint32_t n_steps) {
     return with_engine(h, [&](uuv::Engine& e) {
         if (!act || !obs || !rew || !done) return fail(UUVSIM_ERR_SIZE, "null buffer");

@@ -316,6 +316,11 @@ void Engine::parse(const std::string& text) {
             if (!v->is_boolean()) throw ConfigError("device.stats must be a bool");
             stats_on_ = v->get<bool>();
         }
+        if (const json* v = opt(*d, "pattern")) {
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "dense") force_dense_ = true;
+            else if (s != "auto") throw ConfigError("device.pattern must be \"auto\" or \"dense\"");
+        }
     } else {
         cudaGetDevice(&device_);
     }
@@ -433,6 +438,28 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     if (off > arena_bytes_) throw RuntimeError("internal: arena too small");
 }
 
+// Structure test for the PatFossen kernels (uuv_model.cuh): every entry outside
+// {diag, (0,4), (4,0), (1,3), (3,1)} of M_RB and M_A is exactly zero, D_lin is
+// diagonal and r_g lies on the body z axis -- for every vehicle in the batch.
+bool Engine::check_fossen() const {
+    auto in_m = [](int i, int j) {
+        return i == j || (i == 0 && j == 4) || (i == 4 && j == 0) || (i == 1 && j == 3) ||
+               (i == 3 && j == 1);
+    };
+    for (const BaseVehicle& v : veh_) {
+        double m_rb[36], m_total[36];
+        mass_matrices(v, m_rb, m_total);
+        if (v.rg[0] != 0.0 || v.rg[1] != 0.0) return false;
+        for (int i = 0; i < 6; ++i)
+            for (int j = 0; j < 6; ++j) {
+                if (!in_m(i, j) && (m_rb[i * 6 + j] != 0.0 || v.added[i * 6 + j] != 0.0))
+                    return false;
+                if (i != j && v.dlin[i * 6 + j] != 0.0) return false;
+            }
+    }
+    return true;
+}
+
 void Engine::activate() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
 
 void Engine::allocate() {
@@ -447,8 +474,8 @@ void Engine::allocate() {
     if (ranges_.enabled) bytes += 2 * align256(N * 4 * sT) + align256(N * 2 * sT);
     size_t free_b = 0, total_b = 0;
     cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const size_t abi = align256(N * n_act_ * 8) + align256(N * obs_dim_ * 8) + align256(N * 8) +
-                       2 * align256(N) + align256(N * 12 * 8);
+    const size_t abi = (align256(N * n_act_ * 8) + align256(N * obs_dim_ * 8) + align256(N * 8)) *
+                           (fp64_ ? 1 : 2) + 2 * align256(N) + align256(N * 12 * 8);
     if (bytes + abi > free_b)
         throw ConfigError("batch.num_envs needs " + std::to_string((bytes + abi) >> 20) +
                           " MiB of device memory, " + std::to_string(free_b >> 20) + " MiB free");
@@ -475,6 +502,15 @@ void Engine::allocate() {
     cuda_check(cudaMalloc(&d_act64_, N * n_act_ * 8), "cudaMalloc(abi act)");
     cuda_check(cudaMalloc(&d_obs64_, N * obs_dim_ * 8), "cudaMalloc(abi obs)");
     cuda_check(cudaMalloc(&d_rew64_, N * 8), "cudaMalloc(abi rew)");
+    if (fp64_) {
+        d_actT_ = d_act64_;
+        d_obsT_ = d_obs64_;
+        d_rewT_ = d_rew64_;
+    } else {
+        cuda_check(cudaMalloc(&d_actT_, N * n_act_ * 4), "cudaMalloc(abi act32)");
+        cuda_check(cudaMalloc(&d_obsT_, N * obs_dim_ * 4), "cudaMalloc(abi obs32)");
+        cuda_check(cudaMalloc(&d_rewT_, N * 4), "cudaMalloc(abi rew32)");
+    }
     cuda_check(cudaMalloc(&d_done_, N), "cudaMalloc(abi done)");
     cuda_check(cudaMalloc(&d_reason_, N), "cudaMalloc(abi reason)");
     cuda_check(cudaMalloc(&d_pack_, N * 12 * 8), "cudaMalloc(abi pack)");
@@ -484,6 +520,7 @@ void Engine::allocate() {
 
 Engine::Engine(const std::string& text) {
     parse(text);
+    fossen_ = !force_dense_ && check_fossen();
     try {
         allocate();
         if (fp64_) {
@@ -506,6 +543,12 @@ Engine::~Engine() { release(); }
 void Engine::release() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     graph_exec_ = nullptr;
+    if (!fp64_) {
+        void* t[] = {d_actT_, d_obsT_, d_rewT_};
+        for (void* b : t)
+            if (b) cudaFree(b);
+    }
+    d_actT_ = d_obsT_ = d_rewT_ = nullptr;
     void* bufs[] = {arena_, traj_, stats_part_, d_act64_, d_obs64_, d_rew64_, d_done_,
                     d_reason_, d_pack_, d_flag_, d_stats_out_};
     for (void* b : bufs)
@@ -535,40 +578,52 @@ void Engine::init_randomization() {   // engine.rs:440-458: per-env sample at cr
 }
 
 // ------------------------------------------------------------------ host ABI face
-void Engine::reset_host(uint64_t seed, double* obs) {
-    activate();
-    if (fp64_) {
-        pd_->seed = seed;
-        cuda_check(Launch<double>::reset<double>(*pd_, obs ? d_obs64_ : nullptr, stream_), "reset");
-    } else {
-        pf_->seed = seed;
-        cuda_check(Launch<float>::reset<double>(*pf_, obs ? d_obs64_ : nullptr, stream_), "reset");
+template <class T> void Engine::reset_host_T(uint64_t seed, double* obs) {
+    EngineP<T>& p = P<T>();
+    p.seed = seed;
+    const size_t n_obs = (size_t)m_ * obs_dim_;
+    cuda_check(Launch<T>::reset(p, obs ? (T*)d_obsT_ : nullptr, stream_), "reset");
+    if (obs) {
+        if (!fp64_) cuda_check(Launch<T>::to_f64((T*)d_obsT_, d_obs64_, n_obs, stream_), "obs cvt");
+        cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_),
+                   "reset D2H");
     }
-    if (obs)
-        cuda_check(cudaMemcpyAsync(obs, d_obs64_, (size_t)m_ * obs_dim_ * 8, cudaMemcpyDeviceToHost,
-                                   stream_), "reset D2H");
     cuda_check(cudaStreamSynchronize(stream_), "reset sync");
 }
 
-void Engine::step_host(const double* act, double* obs, double* rew, uint8_t* done,
-                       int8_t* reason) {
+void Engine::reset_host(uint64_t seed, double* obs) {
     activate();
-    const size_t N = (size_t)m_;
-    cuda_check(cudaMemcpyAsync(d_act64_, act, N * n_act_ * 8, cudaMemcpyHostToDevice, stream_),
+    if (fp64_) reset_host_T<double>(seed, obs);
+    else reset_host_T<float>(seed, obs);
+}
+
+// uuvsim_step: H2D actions -> (convert) -> fused step -> (convert) -> D2H outputs
+template <class T>
+void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* done,
+                         int8_t* reason) {
+    const size_t N = (size_t)m_, n_act = N * n_act_, n_obs = N * obs_dim_;
+    cuda_check(cudaMemcpyAsync(d_act64_, act, n_act * 8, cudaMemcpyHostToDevice, stream_),
                "step H2D");
-    const bool track = task_.kind != 0, dr = ranges_.enabled;
-    if (fp64_)
-        cuda_check(Launch<double>::step<double>(*pd_, track, dr, d_act64_, d_obs64_, d_rew64_,
-                                                d_done_, d_reason_, stream_), "step");
-    else
-        cuda_check(Launch<float>::step<double>(*pf_, track, dr, d_act64_, d_obs64_, d_rew64_,
-                                               d_done_, d_reason_, stream_), "step");
-    cuda_check(cudaMemcpyAsync(obs, d_obs64_, N * obs_dim_ * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
+    if (!fp64_) cuda_check(Launch<T>::from_f64(d_act64_, (T*)d_actT_, n_act, stream_), "act cvt");
+    cuda_check(Launch<T>::step(P<T>(), task_.kind != 0, ranges_.enabled, fossen_, (T*)d_actT_,
+                               (T*)d_obsT_, (T*)d_rewT_, d_done_, d_reason_, stream_), "step");
+    if (!fp64_) {
+        cuda_check(Launch<T>::to_f64((T*)d_obsT_, d_obs64_, n_obs, stream_), "obs cvt");
+        cuda_check(Launch<T>::to_f64((T*)d_rewT_, d_rew64_, N, stream_), "rew cvt");
+    }
+    cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
     cuda_check(cudaMemcpyAsync(rew, d_rew64_, N * 8, cudaMemcpyDeviceToHost, stream_), "rew D2H");
     cuda_check(cudaMemcpyAsync(done, d_done_, N, cudaMemcpyDeviceToHost, stream_), "done D2H");
     if (reason)
         cuda_check(cudaMemcpyAsync(reason, d_reason_, N, cudaMemcpyDeviceToHost, stream_), "reason D2H");
     cuda_check(cudaStreamSynchronize(stream_), "step sync");
+}
+
+void Engine::step_host(const double* act, double* obs, double* rew, uint8_t* done,
+                       int8_t* reason) {
+    activate();
+    if (fp64_) step_host_T<double>(act, obs, rew, done, reason);
+    else step_host_T<float>(act, obs, rew, done, reason);
 }
 
 void Engine::states_host(double* out) {
@@ -644,38 +699,44 @@ void Engine::stats_host(double* out, bool clear) {
 }
 
 // ------------------------------------------------------------------ device face
-void Engine::dev_step(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+void Engine::dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8_t* reason,
                       cudaStream_t st) {
     const bool track = task_.kind != 0, dr = ranges_.enabled;
-    if (fp64_) cuda_check(Launch<double>::step<float>(*pd_, track, dr, act, obs, rew, done, reason, st), "dev_step");
-    else cuda_check(Launch<float>::step<float>(*pf_, track, dr, act, obs, rew, done, reason, st), "dev_step");
+    if (fp64_)
+        cuda_check(Launch<double>::step(*pd_, track, dr, fossen_, (const double*)act,
+                                        (double*)obs, (double*)rew, done, reason, st), "dev_step");
+    else
+        cuda_check(Launch<float>::step(*pf_, track, dr, fossen_, (const float*)act, (float*)obs,
+                                       (float*)rew, done, reason, st), "dev_step");
 }
 
-void Engine::dev_reset(uint64_t seed, float* obs, cudaStream_t st) {
+void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
     if (fp64_) {
         pd_->seed = seed;
-        cuda_check(Launch<double>::reset<float>(*pd_, obs, st), "dev_reset");
+        cuda_check(Launch<double>::reset(*pd_, (double*)obs, st), "dev_reset");
     } else {
         pf_->seed = seed;
-        cuda_check(Launch<float>::reset<float>(*pf_, obs, st), "dev_reset");
+        cuda_check(Launch<float>::reset(*pf_, (float*)obs, st), "dev_reset");
     }
 }
 
-void Engine::dev_observe(float* obs, cudaStream_t st) {
-    if (fp64_) cuda_check(Launch<double>::observe<float>(*pd_, obs, st), "dev_observe");
-    else cuda_check(Launch<float>::observe<float>(*pf_, obs, st), "dev_observe");
+void Engine::dev_observe(void* obs, cudaStream_t st) {
+    if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
+    else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
 }
 
-void Engine::dev_bench_actions(float* act, cudaStream_t st) {
+void Engine::dev_bench_actions(void* act, cudaStream_t st) {
     const uint64_t seed = fp64_ ? pd_->seed : pf_->seed;
-    cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_, act, nullptr, st), "bench_actions");
+    cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_,
+                                    fp64_ ? nullptr : (float*)act,
+                                    fp64_ ? (double*)act : nullptr, st), "bench_actions");
 }
 
 void Engine::dev_stats(double* out, bool clear, cudaStream_t st) {
     cuda_check(launch_stats_reduce(stats_part_, nblk_, out, clear ? 1 : 0, st), "dev_stats");
 }
 
-void Engine::graph_capture(const float* act, float* obs, float* rew, uint8_t* done,
+void Engine::graph_capture(const void* act, void* obs, void* rew, uint8_t* done,
                            int8_t* reason, int n_steps) {
     activate();
     if (graph_exec_) {
@@ -711,8 +772,8 @@ void Engine::synchronize() {
 std::string Engine::info() const {
     cudaFuncAttributes a{};
     const bool track = task_.kind != 0, dr = ranges_.enabled, mix = veh_.size() > 1;
-    if (fp64_) Launch<double>::step_attrs(&a, track, dr, mix);
-    else Launch<float>::step_attrs(&a, track, dr, mix);
+    if (fp64_) Launch<double>::step_attrs(&a, track, dr, fossen_, mix);
+    else Launch<float>::step_attrs(&a, track, dr, fossen_, mix);
     json j = {
         {"engine", "paper_2410_14117_b200"},
         {"abi_version", 1},
@@ -726,6 +787,7 @@ std::string Engine::info() const {
         {"task_kind", task_.kind},
         {"n_vehicles", veh_.size()},
         {"randomization", ranges_.enabled},
+        {"pattern", fossen_ ? "fossen" : "dense"},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},

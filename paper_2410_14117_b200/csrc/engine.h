@@ -80,14 +80,17 @@ public:
     void dr_factors_host(double* out);     // [M][10]
     void stats_host(double* out, bool clear);
 
-    // device face (zero-copy, stream-ordered, graph-capturable)
-    void dev_step(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+    // device face (zero-copy, stream-ordered, graph-capturable).  Element type of
+    // act/obs/rew is the engine precision: f32 for fp32 engines, f64 for fp64.
+    bool is_fp64() const { return fp64_; }
+    bool fossen() const { return fossen_; }
+    void dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8_t* reason,
                   cudaStream_t st);
-    void dev_reset(uint64_t seed, float* obs, cudaStream_t st);
-    void dev_observe(float* obs, cudaStream_t st);
-    void dev_bench_actions(float* act, cudaStream_t st);
+    void dev_reset(uint64_t seed, void* obs, cudaStream_t st);
+    void dev_observe(void* obs, cudaStream_t st);
+    void dev_bench_actions(void* act, cudaStream_t st);
     void dev_stats(double* out, bool clear, cudaStream_t st);
-    void graph_capture(const float* act, float* obs, float* rew, uint8_t* done, int8_t* reason,
+    void graph_capture(const void* act, void* obs, void* rew, uint8_t* done, int8_t* reason,
                        int n_steps);
     void graph_launch(cudaStream_t st);
     void synchronize();
@@ -102,6 +105,10 @@ private:
     void init_randomization();
     template <class T> EngineP<T>& P();
     template <class T> void fill_params(EngineP<T>& p);
+    template <class T> void step_host_T(const double* act, double* obs, double* rew,
+                                        uint8_t* done, int8_t* reason);
+    template <class T> void reset_host_T(uint64_t seed, double* obs);
+    bool check_fossen() const;
 
     // config
     uint64_t seed_ = 0;
@@ -110,6 +117,8 @@ private:
     int obs_dim_ = 0, n_act_ = 0;
     bool fp64_ = false;
     bool stats_on_ = true;
+    bool fossen_ = false;
+    bool force_dense_ = false;
     int device_ = 0;
     std::vector<BaseVehicle> veh_;
     std::vector<int64_t> mix_;
@@ -126,7 +135,10 @@ private:
     void* traj_ = nullptr;
     double* stats_part_ = nullptr;
     int nblk_ = 0;
-    // ABI staging (f64 host layout)
+    // ABI staging (f64 host layout; fp32 engines convert on device)
+    void* d_actT_ = nullptr;
+    void* d_obsT_ = nullptr;
+    void* d_rewT_ = nullptr;
     double* d_act64_ = nullptr;
     double* d_obs64_ = nullptr;
     double* d_rew64_ = nullptr;

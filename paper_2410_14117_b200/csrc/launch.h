@@ -11,16 +11,19 @@ namespace uuv {
 constexpr int BLOCK = 128;   // threads per block of the env kernels (one env per thread)
 
 template <class T> struct Launch {
-    template <class IO>
-    static cudaError_t step(const EngineP<T>& p, bool track, bool dr, const IO* act, IO* obs,
-                            IO* rew, uint8_t* done, int8_t* reason, cudaStream_t st);
-    template <class IO> static cudaError_t reset(const EngineP<T>& p, IO* obs, cudaStream_t st);
-    template <class IO> static cudaError_t observe(const EngineP<T>& p, IO* obs, cudaStream_t st);
+    // one fused step; fossen selects the structure-specialised variant
+    static cudaError_t step(const EngineP<T>& p, bool track, bool dr, bool fossen, const T* act,
+                            T* obs, T* rew, uint8_t* done, int8_t* reason, cudaStream_t st);
+    static cudaError_t reset(const EngineP<T>& p, T* obs, cudaStream_t st);
+    static cudaError_t observe(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);
     static cudaError_t pack_states(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
-    static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool mix);
+    static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
+                                  bool mix);
+    static cudaError_t to_f64(const T* in, double* out, size_t n, cudaStream_t st);
+    static cudaError_t from_f64(const double* in, T* out, size_t n, cudaStream_t st);
 };
 
 cudaError_t launch_bench_actions(uint64_t seed, uint64_t env_offset, int n_env, int act_dim,

@@ -14,16 +14,18 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "uuv_model.cuh"
 #include "launch.h"
 
 namespace uuv {
 
 
-template <class T, bool TRACK, bool DR, int SLOT, class IO>
+template <class T, bool TRACK, bool DR, int SLOT, class Pat>
 __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
-                                         const IO* __restrict__ act, IO* __restrict__ obs,
-                                         IO* __restrict__ rew, uint8_t* __restrict__ done,
+                                         const T* __restrict__ act, T* __restrict__ obs,
+                                         T* __restrict__ rew, uint8_t* __restrict__ done,
                                          int8_t* __restrict__ reason, float& st_rew,
                                          int& st_reason, float& st_epret, int& st_eplen,
                                          int& st_err) {
@@ -37,16 +39,16 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
     if constexpr (DR) {
         const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
         const V2<T> d2 = p.dr2[e];
-        build_env<T>(V, d0, d1, d2, E);
+        build_env<T, Pat>(V, d0, d1, d2, E);
     }
     T tau[6];
-    wrench<T, DR, IO>(V, E, act + (size_t)e * p.act_dim, tau);
+    wrench<T, DR>(V, E, act + (size_t)e * p.act_dim, tau);
 
     bool failed = false;
     const T dt = tk.sub_dt;
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
-        if (!substep<T, DR>(V, E, s, tau, dt)) {
+        if (!substep<T, DR, Pat>(V, E, s, tau, dt)) {
             failed = true;
             break;
         }
@@ -101,32 +103,31 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
     p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
 
     // observation (post-reset for finished envs, batch.py:106-118)
-    IO* row = obs + (size_t)e * tk.obs_dim;
+    T* row = obs + (size_t)e * tk.obs_dim;
     if constexpr (!TRACK) {
-        V4<IO>* o4 = reinterpret_cast<V4<IO>*>(row);
-        o4[0] = V4<IO>{(IO)(tk.target[0] - s[0]), (IO)(tk.target[1] - s[1]),
-                       (IO)(tk.target[2] - s[2]), (IO)wrap_t<T>(tk.target[3] - s[3])};
-        o4[1] = V4<IO>{(IO)wrap_t<T>(tk.target[4] - s[4]), (IO)wrap_t<T>(tk.target[5] - s[5]),
-                       (IO)s[6], (IO)s[7]};
-        o4[2] = V4<IO>{(IO)s[8], (IO)s[9], (IO)s[10], (IO)s[11]};
+        V4<T>* o4 = reinterpret_cast<V4<T>*>(row);
+        o4[0] = V4<T>{tk.target[0] - s[0], tk.target[1] - s[1], tk.target[2] - s[2],
+                      wrap_t<T>(tk.target[3] - s[3])};
+        o4[1] = V4<T>{wrap_t<T>(tk.target[4] - s[4]), wrap_t<T>(tk.target[5] - s[5]), s[6], s[7]};
+        o4[2] = V4<T>{s[8], s[9], s[10], s[11]};
     } else {
-        V2<IO>* o2 = reinterpret_cast<V2<IO>*>(row);
-        const IO ephi = (IO)wrap_t<T>(T(0) - s[3]);
-        const IO eth = (IO)wrap_t<T>(T(0) - s[4]);
+        V2<T>* o2 = reinterpret_cast<V2<T>*>(row);
+        const T ephi = wrap_t<T>(T(0) - s[3]);
+        const T eth = wrap_t<T>(T(0) - s[4]);
 #pragma unroll 1
         for (int k = 1; k <= tk.lookahead; ++k) {
             const V4<T> r = tk.traj[min(nstep + k, tab_last)];
-            V2<IO>* q = o2 + 3 * (k - 1);
-            q[0] = V2<IO>{(IO)(r.x - s[0]), (IO)(r.y - s[1])};
-            q[1] = V2<IO>{(IO)(r.z - s[2]), ephi};
-            q[2] = V2<IO>{eth, (IO)wrap_t<T>(r.w - s[5])};
+            V2<T>* q = o2 + 3 * (k - 1);
+            q[0] = V2<T>{r.x - s[0], r.y - s[1]};
+            q[1] = V2<T>{r.z - s[2], ephi};
+            q[2] = V2<T>{eth, wrap_t<T>(r.w - s[5])};
         }
-        V2<IO>* q = o2 + 3 * tk.lookahead;
-        q[0] = V2<IO>{(IO)s[6], (IO)s[7]};
-        q[1] = V2<IO>{(IO)s[8], (IO)s[9]};
-        q[2] = V2<IO>{(IO)s[10], (IO)s[11]};
+        V2<T>* q = o2 + 3 * tk.lookahead;
+        q[0] = V2<T>{s[6], s[7]};
+        q[1] = V2<T>{s[8], s[9]};
+        q[2] = V2<T>{s[10], s[11]};
     }
-    rew[e] = (IO)reward;
+    rew[e] = reward;
     done[e] = rc >= 0 ? 1 : 0;
     if (reason) reason[e] = (int8_t)rc;
     st_rew = (float)reward;
@@ -172,10 +173,10 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, bool acti
     }
 }
 
-template <class T, bool TRACK, bool DR, bool MIX, class IO>
+template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BLOCK)
-k_step(const __grid_constant__ EngineP<T> p, const IO* __restrict__ act, IO* __restrict__ obs,
-       IO* __restrict__ rew, uint8_t* __restrict__ done, int8_t* __restrict__ reason) {
+k_step(const __grid_constant__ EngineP<T> p, const T* __restrict__ act, T* __restrict__ obs,
+       T* __restrict__ rew, uint8_t* __restrict__ done, int8_t* __restrict__ reason) {
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     const bool active = e < p.n_env;
     float st_rew = 0.f, st_epret = 0.f;
@@ -185,10 +186,10 @@ k_step(const __grid_constant__ EngineP<T> p, const IO* __restrict__ act, IO* __r
         bool slot1 = false;
         if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
         if (!slot1)
-            step_env<T, TRACK, DR, 0, IO>(p, e, g, act, obs, rew, done, reason, st_rew,
+            step_env<T, TRACK, DR, 0, Pat>(p, e, g, act, obs, rew, done, reason, st_rew,
                                           st_reason, st_epret, st_eplen, st_err);
         else if constexpr (MIX)
-            step_env<T, TRACK, DR, 1, IO>(p, e, g, act, obs, rew, done, reason, st_rew,
+            step_env<T, TRACK, DR, 1, Pat>(p, e, g, act, obs, rew, done, reason, st_rew,
                                           st_reason, st_epret, st_eplen, st_err);
     }
     if (p.stats_on) block_stats(p.stats, active, st_rew, st_reason, st_epret, st_eplen, st_err);
@@ -306,34 +307,35 @@ __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restri
 
 // ------------------------------------------------------------------ launchers
 template <class T>
-template <class IO>
-cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, const IO* act, IO* obs,
-                            IO* rew, uint8_t* done, int8_t* reason, cudaStream_t st) {
+cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, const T* act,
+                            T* obs, T* rew, uint8_t* done, int8_t* reason, cudaStream_t st) {
     const dim3 grid((p.n_env + BLOCK - 1) / BLOCK);
     const bool mix = p.n_veh > 1;
-#define UUV_L(TR, D, M) k_step<T, TR, D, M, IO><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
+#define UUV_L(TR, D, M, PAT) \
+    k_step<T, TR, D, M, PAT><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
+#define UUV_LP(TR, D, M) \
+    if (fossen) UUV_L(TR, D, M, PatFossen); else UUV_L(TR, D, M, PatDense)
     if (track) {
-        if (dr) { if (mix) UUV_L(true, true, true); else UUV_L(true, true, false); }
-        else { if (mix) UUV_L(true, false, true); else UUV_L(true, false, false); }
+        if (dr) { if (mix) UUV_LP(true, true, true); else UUV_LP(true, true, false); }
+        else { if (mix) UUV_LP(true, false, true); else UUV_LP(true, false, false); }
     } else {
-        if (dr) { if (mix) UUV_L(false, true, true); else UUV_L(false, true, false); }
-        else { if (mix) UUV_L(false, false, true); else UUV_L(false, false, false); }
+        if (dr) { if (mix) UUV_LP(false, true, true); else UUV_LP(false, true, false); }
+        else { if (mix) UUV_LP(false, false, true); else UUV_LP(false, false, false); }
     }
+#undef UUV_LP
 #undef UUV_L
     return cudaGetLastError();
 }
 
 template <class T>
-template <class IO>
-cudaError_t Launch<T>::reset(const EngineP<T>& p, IO* obs, cudaStream_t st) {
-    k_reset<T, IO><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p, obs);
+cudaError_t Launch<T>::reset(const EngineP<T>& p, T* obs, cudaStream_t st) {
+    k_reset<T, T><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p, obs);
     return cudaGetLastError();
 }
 
 template <class T>
-template <class IO>
-cudaError_t Launch<T>::observe(const EngineP<T>& p, IO* obs, cudaStream_t st) {
-    k_observe<T, IO><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p, obs);
+cudaError_t Launch<T>::observe(const EngineP<T>& p, T* obs, cudaStream_t st) {
+    k_observe<T, T><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p, obs);
     return cudaGetLastError();
 }
 
@@ -362,33 +364,45 @@ cudaError_t Launch<T>::pack_dr(const EngineP<T>& p, double* out, cudaStream_t st
 }
 
 template <class T>
-cudaError_t Launch<T>::step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool mix) {
-#define UUV_A(TR, D, M) return cudaFuncGetAttributes(a, k_step<T, TR, D, M, float>)
+cudaError_t Launch<T>::step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
+                                  bool mix) {
+#define UUV_A(TR, D, M, PAT) return cudaFuncGetAttributes(a, k_step<T, TR, D, M, PAT>)
+#define UUV_AP(TR, D, M) \
+    if (fossen) UUV_A(TR, D, M, PatFossen); else UUV_A(TR, D, M, PatDense)
     if (track) {
-        if (dr) { if (mix) UUV_A(true, true, true); else UUV_A(true, true, false); }
-        else { if (mix) UUV_A(true, false, true); else UUV_A(true, false, false); }
+        if (dr) { if (mix) UUV_AP(true, true, true); else UUV_AP(true, true, false); }
+        else { if (mix) UUV_AP(true, false, true); else UUV_AP(true, false, false); }
     } else {
-        if (dr) { if (mix) UUV_A(false, true, true); else UUV_A(false, true, false); }
-        else { if (mix) UUV_A(false, false, true); else UUV_A(false, false, false); }
+        if (dr) { if (mix) UUV_AP(false, true, true); else UUV_AP(false, true, false); }
+        else { if (mix) UUV_AP(false, false, true); else UUV_AP(false, false, false); }
     }
+#undef UUV_AP
 #undef UUV_A
+}
+
+template <class A, class B>
+__global__ void k_convert(const A* __restrict__ in, B* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = (B)in[i];
+}
+
+template <class T>
+cudaError_t Launch<T>::to_f64(const T* in, double* out, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+    k_convert<T, double><<<blocks, 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::from_f64(const double* in, T* out, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+    k_convert<double, T><<<blocks, 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
 }
 
 }  // namespace uuv
 
-#define UUV_INSTANTIATE(T)                                                                   \
-    template struct uuv::Launch<T>;                                                          \
-    template cudaError_t uuv::Launch<T>::step<float>(const uuv::EngineP<T>&, bool, bool,     \
-                                                     const float*, float*, float*, uint8_t*, \
-                                                     int8_t*, cudaStream_t);                 \
-    template cudaError_t uuv::Launch<T>::step<double>(const uuv::EngineP<T>&, bool, bool,    \
-                                                      const double*, double*, double*,       \
-                                                      uint8_t*, int8_t*, cudaStream_t);      \
-    template cudaError_t uuv::Launch<T>::reset<float>(const uuv::EngineP<T>&, float*,        \
-                                                      cudaStream_t);                         \
-    template cudaError_t uuv::Launch<T>::reset<double>(const uuv::EngineP<T>&, double*,      \
-                                                       cudaStream_t);                        \
-    template cudaError_t uuv::Launch<T>::observe<float>(const uuv::EngineP<T>&, float*,      \
-                                                        cudaStream_t);                       \
-    template cudaError_t uuv::Launch<T>::observe<double>(const uuv::EngineP<T>&, double*,    \
-                                                         cudaStream_t);
+#define UUV_INSTANTIATE(T) template struct uuv::Launch<T>;
