@@ -363,6 +363,8 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
             V.rb64[k] = v.rb[k];
         }
         V.weight64 = v.weight;
+        V.wb = (T)(v.weight - v.buoyancy);
+        for (int k = 0; k < 3; ++k) V.hm[k] = (T)(v.weight * v.rg[k] - v.buoyancy * v.rb[k]);
         const int n = (int)v.kmax.size();
         V.n_thr = n;
         for (int i = 0; i < n; ++i) {   // thrusters.py:81-94 / engine.rs:260-271

@@ -109,6 +109,8 @@ template <class T> struct VehP {
     T dquad[6];
     T weight, buoyancy;
     T rg[3], rb[3];
+    T wb;            // W - B            (fused fp32 restoring term)
+    T hm[3];         // W r_g - B r_b    (restoring moment = hm x e, e = R^T z)
     T alloc[6 * MAX_THR];   // 6 x MAX_THR, zero-padded columns
     T kmax[MAX_THR];
     int32_t curve[MAX_THR]; // 0 linear, 1 quadratic_signed

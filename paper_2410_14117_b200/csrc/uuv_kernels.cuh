@@ -46,7 +46,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
 
     bool failed = false;
     const T dt = tk.sub_dt;
-#pragma unroll 1
+#pragma unroll 2
     for (int k = 0; k < tk.n_substeps; ++k) {
         if (!substep<T, DR, Pat>(V, E, s, tau, dt)) {
             failed = true;
@@ -91,9 +91,11 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
                 p.param_ctr[e] = pc;
             }
         }
-        uint64_t ctr = p.reset_ctr[e];
-        reset_state<T>(tk, seed, g, ctr, s);
-        p.reset_ctr[e] = ctr;
+        const uint64_t ctr = p.reset_ctr[e];
+        const State12<T> rs = reset_state<T>(tk, seed, g, ctr);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) s[i] = rs.v[i];
+        p.reset_ctr[e] = ctr + 6;
         nstep = 0;
     }
     p.ep_ret[e] = er;
@@ -107,20 +109,20 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
     if constexpr (!TRACK) {
         V4<T>* o4 = reinterpret_cast<V4<T>*>(row);
         o4[0] = V4<T>{tk.target[0] - s[0], tk.target[1] - s[1], tk.target[2] - s[2],
-                      wrap_t<T>(tk.target[3] - s[3])};
-        o4[1] = V4<T>{wrap_t<T>(tk.target[4] - s[4]), wrap_t<T>(tk.target[5] - s[5]), s[6], s[7]};
+                      obs_wrap<T>(tk.target[3] - s[3])};
+        o4[1] = V4<T>{obs_wrap<T>(tk.target[4] - s[4]), obs_wrap<T>(tk.target[5] - s[5]), s[6], s[7]};
         o4[2] = V4<T>{s[8], s[9], s[10], s[11]};
     } else {
         V2<T>* o2 = reinterpret_cast<V2<T>*>(row);
-        const T ephi = wrap_t<T>(T(0) - s[3]);
-        const T eth = wrap_t<T>(T(0) - s[4]);
+        const T ephi = obs_wrap<T>(T(0) - s[3]);
+        const T eth = obs_wrap<T>(T(0) - s[4]);
 #pragma unroll 1
         for (int k = 1; k <= tk.lookahead; ++k) {
             const V4<T> r = tk.traj[min(nstep + k, tab_last)];
             V2<T>* q = o2 + 3 * (k - 1);
             q[0] = V2<T>{r.x - s[0], r.y - s[1]};
             q[1] = V2<T>{r.z - s[2], ephi};
-            q[2] = V2<T>{eth, wrap_t<T>(r.w - s[5])};
+            q[2] = V2<T>{eth, obs_wrap<T>(r.w - s[5])};
         }
         V2<T>* q = o2 + 3 * tk.lookahead;
         q[0] = V2<T>{s[6], s[7]};
@@ -205,9 +207,9 @@ __device__ __forceinline__ void observe_env(const EngineP<T>& p, int e, const T 
         row[0] = (IO)(tk.target[0] - s[0]);
         row[1] = (IO)(tk.target[1] - s[1]);
         row[2] = (IO)(tk.target[2] - s[2]);
-        row[3] = (IO)wrap_t<T>(tk.target[3] - s[3]);
-        row[4] = (IO)wrap_t<T>(tk.target[4] - s[4]);
-        row[5] = (IO)wrap_t<T>(tk.target[5] - s[5]);
+        row[3] = (IO)obs_wrap<T>(tk.target[3] - s[3]);
+        row[4] = (IO)obs_wrap<T>(tk.target[4] - s[4]);
+        row[5] = (IO)obs_wrap<T>(tk.target[5] - s[5]);
         for (int i = 6; i < 12; ++i) row[i] = (IO)s[i];
     } else {
         const int tab_last = tk.episode_len + tk.lookahead;
@@ -217,9 +219,9 @@ __device__ __forceinline__ void observe_env(const EngineP<T>& p, int e, const T 
             row[n++] = (IO)(r.x - s[0]);
             row[n++] = (IO)(r.y - s[1]);
             row[n++] = (IO)(r.z - s[2]);
-            row[n++] = (IO)wrap_t<T>(T(0) - s[3]);
-            row[n++] = (IO)wrap_t<T>(T(0) - s[4]);
-            row[n++] = (IO)wrap_t<T>(r.w - s[5]);
+            row[n++] = (IO)obs_wrap<T>(T(0) - s[3]);
+            row[n++] = (IO)obs_wrap<T>(T(0) - s[4]);
+            row[n++] = (IO)obs_wrap<T>(r.w - s[5]);
         }
         for (int i = 6; i < 12; ++i) row[n++] = (IO)s[i];
     }
@@ -232,10 +234,10 @@ __global__ void __launch_bounds__(BLOCK) k_reset(const __grid_constant__ EngineP
     if (e >= p.n_env) return;
     const uint64_t g = p.env_offset + (uint64_t)e;
     if (e == 0) *p.seed_dev = p.seed;
-    uint64_t ctr = 0;   // reset_all rewinds the reset stream (batch.py:80-83)
-    T s[12];
-    reset_state<T>(p.task, p.seed, g, ctr, s);
-    p.reset_ctr[e] = ctr;
+    // reset_all rewinds the reset stream (batch.py:80-83)
+    const State12<T> rs = reset_state<T>(p.task, p.seed, g, 0);
+    const T* s = rs.v;
+    p.reset_ctr[e] = 6;
     p.step[e] = 0;
     p.ep_ret[e] = 0.0f;
     p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
