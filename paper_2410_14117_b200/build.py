@@ -64,24 +64,29 @@ def _stale(out: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines=()) -> Path:
+    """Compile + link.  ``out``/``defines`` build an experimental variant (own obj dir)."""
     cuda = _cuda_home()
+    lib = Path(out) if out else LIB
+    objdir = (lib.parent / "obj") if out else OBJDIR
     nvcc = str(cuda / "bin" / "nvcc")
     cxx = _host_cxx()
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+    objdir.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     headers = sorted(glob.glob(str(CSRC / "*.h")) + glob.glob(str(CSRC / "*.cuh")) +
                      [str(INCLUDE / "uuvsim.h")])
     common_nv = [nvcc, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-ccbin", cxx,
-                 "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills", "-I", str(CSRC)]
+                 "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills", "-I", str(CSRC), *dflags]
     jobs = [
-        (OBJDIR / "k_f32.o", [*common_nv, "-c", str(CSRC / "k_f32.cu")], [CSRC / "k_f32.cu"]),
-        (OBJDIR / "k_f64.o", [*common_nv, "-fmad=false", "-c", str(CSRC / "k_f64.cu")],
+        (objdir / "k_f32.o", [*common_nv, "-c", str(CSRC / "k_f32.cu")], [CSRC / "k_f32.cu"]),
+        (objdir / "k_f64.o", [*common_nv, "-fmad=false", "-c", str(CSRC / "k_f64.cu")],
          [CSRC / "k_f64.cu"]),
     ]
     host = [cxx, "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wno-unused-function",
             "-I", str(cuda / "include"), "-I", str(_nlohmann_include()), "-I", str(CSRC), "-c"]
     for name in ("engine.cpp", "capi.cpp"):
-        jobs.append((OBJDIR / (name[:-4] + ".o"), [*host, str(CSRC / name)], [CSRC / name]))
+        jobs.append((objdir / (name[:-4] + ".o"), [*host, *dflags, str(CSRC / name)], [CSRC / name]))
     todo = [(o, cmd + ["-o", str(o)]) for o, cmd, src in jobs
             if force or _stale(o, [*src, *headers])]
 
@@ -99,15 +104,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             if msg and verbose:
                 print(msg)
     objs = [str(o) for o, _, _ in jobs]
-    if force or todo or _stale(LIB, objs):
-        cmd = [nvcc, "-shared", *ARCH, "-ccbin", cxx, "-o", str(LIB), *objs,
+    if force or todo or _stale(lib, objs):
+        cmd = [nvcc, "-shared", *ARCH, "-ccbin", cxx, "-o", str(lib), *objs,
                "-Xlinker", "--exclude-libs,ALL"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    p = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(p)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None, help="variant library path (own obj dir)")
+    ap.add_argument("-D", action="append", default=[], help="preprocessor define")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=a.D))

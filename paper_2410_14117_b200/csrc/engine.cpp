@@ -316,6 +316,13 @@ void Engine::parse(const std::string& text) {
             if (!v->is_boolean()) throw ConfigError("device.stats must be a bool");
             stats_on_ = v->get<bool>();
         }
+        if (const json* v = opt(*d, "pair")) {
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "auto") pair_mode_ = -1;
+            else if (s == "on") pair_mode_ = 1;
+            else if (s == "off") pair_mode_ = 0;
+            else throw ConfigError("device.pair must be \"auto\", \"on\" or \"off\"");
+        }
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "dense") force_dense_ = true;
@@ -418,6 +425,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.act_dim = n_act_;
     p.stats_on = stats_on_ ? 1 : 0;
     p.stats = stats_part_;
+    p.vpack = d_vpack_;
 
     // device buffers carved from the arena
     char* a = static_cast<char*>(arena_);
@@ -517,12 +525,43 @@ void Engine::allocate() {
     cuda_check(cudaMalloc(&d_reason_, N), "cudaMalloc(abi reason)");
     cuda_check(cudaMalloc(&d_pack_, N * 12 * 8), "cudaMalloc(abi pack)");
     cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "cudaMalloc(flag)");
+    {   // fp32 register pack per vehicle (uuv_model.cuh RegPack layout)
+        std::vector<float> pk((size_t)MAX_VEH * PACK_F4 * 4, 0.0f);
+        for (size_t vi = 0; vi < veh_.size(); ++vi) {
+            const BaseVehicle& v = veh_[vi];
+            double m_rb[36], m_total[36], L[36];
+            mass_matrices(v, m_rb, m_total);
+            cholesky6(m_total, L);
+            const double dt = task_.control_dt / (double)task_.n_substeps;
+            const double vals[40] = {
+                m_total[0], m_total[4], m_total[7], m_total[9],
+                m_total[14], m_total[19], m_total[21], m_total[24],
+                m_total[28], m_total[35], L[3 * 6 + 1], L[4 * 6 + 0],
+                1.0 / L[0], 1.0 / L[7], 1.0 / L[14], 1.0 / L[21],
+                1.0 / L[28], 1.0 / L[35], v.dquad[0], v.dquad[1],
+                v.dquad[2], v.dquad[3], v.dquad[4], v.dquad[5],
+                v.dlin[0], v.dlin[7], v.dlin[14], v.dlin[21],
+                v.dlin[28], v.dlin[35], v.weight - v.buoyancy,
+                v.weight * v.rg[0] - v.buoyancy * v.rb[0],
+                v.weight * v.rg[1] - v.buoyancy * v.rb[1],
+                v.weight * v.rg[2] - v.buoyancy * v.rb[2], dt, 0.0,
+                0.636619772367581343, 0.159154943091895335769, -1.9515295891e-4,
+                2.443315711809948e-5};
+            for (int k = 0; k < 40; ++k) pk[vi * PACK_F4 * 4 + k] = (float)vals[k];
+        }
+        cuda_check(cudaMalloc(&d_vpack_, pk.size() * sizeof(float)), "cudaMalloc(vpack)");
+        cuda_check(cudaMemcpy(d_vpack_, pk.data(), pk.size() * sizeof(float), cudaMemcpyHostToDevice),
+                   "vpack");
+    }
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
 }
 
 Engine::Engine(const std::string& text) {
     parse(text);
     fossen_ = !force_dense_ && check_fossen();
+    // two envs per thread pays off once the paired grid still fills every SM
+    const bool pair_ok = fossen_ && !fp64_ && !ranges_.enabled;
+    pair_ = pair_ok && (pair_mode_ == 1 || (pair_mode_ < 0 && m_ >= PAIR_AUTO_MIN_ENVS));
     try {
         allocate();
         if (fp64_) {
@@ -552,7 +591,7 @@ void Engine::release() {
     }
     d_actT_ = d_obsT_ = d_rewT_ = nullptr;
     void* bufs[] = {arena_, traj_, stats_part_, d_act64_, d_obs64_, d_rew64_, d_done_,
-                    d_reason_, d_pack_, d_flag_, d_stats_out_};
+                    d_reason_, d_pack_, d_flag_, d_stats_out_, d_vpack_};
     for (void* b : bufs)
         if (b) cudaFree(b);
     arena_ = traj_ = nullptr;
@@ -560,6 +599,7 @@ void Engine::release() {
     d_done_ = nullptr;
     d_reason_ = nullptr;
     d_flag_ = nullptr;
+    d_vpack_ = nullptr;
     if (stream_) cudaStreamDestroy(stream_);
     stream_ = nullptr;
 }
@@ -607,7 +647,7 @@ void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* d
     cuda_check(cudaMemcpyAsync(d_act64_, act, n_act * 8, cudaMemcpyHostToDevice, stream_),
                "step H2D");
     if (!fp64_) cuda_check(Launch<T>::from_f64(d_act64_, (T*)d_actT_, n_act, stream_), "act cvt");
-    cuda_check(Launch<T>::step(P<T>(), task_.kind != 0, ranges_.enabled, fossen_, (T*)d_actT_,
+    cuda_check(Launch<T>::step(P<T>(), task_.kind != 0, ranges_.enabled, fossen_, pair_, (T*)d_actT_,
                                (T*)d_obsT_, (T*)d_rewT_, d_done_, d_reason_, stream_), "step");
     if (!fp64_) {
         cuda_check(Launch<T>::to_f64((T*)d_obsT_, d_obs64_, n_obs, stream_), "obs cvt");
@@ -705,10 +745,10 @@ void Engine::dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8
                       cudaStream_t st) {
     const bool track = task_.kind != 0, dr = ranges_.enabled;
     if (fp64_)
-        cuda_check(Launch<double>::step(*pd_, track, dr, fossen_, (const double*)act,
+        cuda_check(Launch<double>::step(*pd_, track, dr, fossen_, pair_, (const double*)act,
                                         (double*)obs, (double*)rew, done, reason, st), "dev_step");
     else
-        cuda_check(Launch<float>::step(*pf_, track, dr, fossen_, (const float*)act, (float*)obs,
+        cuda_check(Launch<float>::step(*pf_, track, dr, fossen_, pair_, (const float*)act, (float*)obs,
                                        (float*)rew, done, reason, st), "dev_step");
 }
 
@@ -774,8 +814,8 @@ void Engine::synchronize() {
 std::string Engine::info() const {
     cudaFuncAttributes a{};
     const bool track = task_.kind != 0, dr = ranges_.enabled, mix = veh_.size() > 1;
-    if (fp64_) Launch<double>::step_attrs(&a, track, dr, fossen_, mix);
-    else Launch<float>::step_attrs(&a, track, dr, fossen_, mix);
+    if (fp64_) Launch<double>::step_attrs(&a, track, dr, fossen_, mix, pair_);
+    else Launch<float>::step_attrs(&a, track, dr, fossen_, mix, pair_);
     json j = {
         {"engine", "paper_2410_14117_b200"},
         {"abi_version", 1},
@@ -790,12 +830,13 @@ std::string Engine::info() const {
         {"n_vehicles", veh_.size()},
         {"randomization", ranges_.enabled},
         {"pattern", fossen_ ? "fossen" : "dense"},
+        {"envs_per_thread", pair_ ? 2 : 1},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},
         {"sm_count", sm_count_},
         {"block", BLOCK},
-        {"grid", nblk_},
+        {"grid", pair_ ? (nblk_ + 1) / 2 : nblk_},
         {"step_kernel_registers", a.numRegs},
         {"step_kernel_local_bytes", a.localSizeBytes},
         {"param_block_bytes", fp64_ ? sizeof(EngineP<double>) : sizeof(EngineP<float>)},

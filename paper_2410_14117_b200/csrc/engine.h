@@ -119,6 +119,8 @@ private:
     bool stats_on_ = true;
     bool fossen_ = false;
     bool force_dense_ = false;
+    int pair_mode_ = -1;      // device.pair: -1 auto, 0 off, 1 on
+    bool pair_ = false;       // two envs per thread (resolved)
     int device_ = 0;
     std::vector<BaseVehicle> veh_;
     std::vector<int64_t> mix_;
@@ -147,6 +149,7 @@ private:
     double* d_pack_ = nullptr;
     int* d_flag_ = nullptr;
     double* d_stats_out_ = nullptr;
+    float4* d_vpack_ = nullptr;
     cudaStream_t stream_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     std::string device_name_;

@@ -9,11 +9,31 @@
 namespace uuv {
 
 constexpr int BLOCK = 128;   // threads per block of the env kernels (one env per thread)
+// register budgets (65536 / (128 * blocks)): measured on B200, see DESIGN.md
+#ifndef UUV_STEP_MIN_BLOCKS
+#define UUV_STEP_MIN_BLOCKS 8      // one env per thread: 64 registers
+#endif
+#ifndef UUV_STEP_MIN_BLOCKS_DR
+#define UUV_STEP_MIN_BLOCKS_DR 6   // with per-env randomised M/L in registers: 85
+#endif
+#ifndef UUV_PAIR_MIN_BLOCKS
+#define UUV_PAIR_MIN_BLOCKS 6      // two envs per thread: 85
+#endif
+constexpr int STEP_MIN_BLOCKS = UUV_STEP_MIN_BLOCKS;
+constexpr int STEP_MIN_BLOCKS_DR = UUV_STEP_MIN_BLOCKS_DR;
+constexpr int PAIR_MIN_BLOCKS = UUV_PAIR_MIN_BLOCKS;
+
+#ifndef UUV_PAIR_AUTO_MIN_ENVS
+#define UUV_PAIR_AUTO_MIN_ENVS 131072
+#endif
+constexpr long PAIR_AUTO_MIN_ENVS = UUV_PAIR_AUTO_MIN_ENVS;
 
 template <class T> struct Launch {
-    // one fused step; fossen selects the structure-specialised variant
-    static cudaError_t step(const EngineP<T>& p, bool track, bool dr, bool fossen, const T* act,
-                            T* obs, T* rew, uint8_t* done, int8_t* reason, cudaStream_t st);
+    // one fused step; fossen selects the structure-specialised variant, pair the
+    // two-envs-per-thread kernel (fp32, Fossen, no randomisation)
+    static cudaError_t step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
+                            const T* act, T* obs, T* rew, uint8_t* done, int8_t* reason,
+                            cudaStream_t st);
     static cudaError_t reset(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t observe(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);
@@ -21,7 +41,7 @@ template <class T> struct Launch {
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
-                                  bool mix);
+                                  bool mix, bool pair);
     static cudaError_t to_f64(const T* in, double* out, size_t n, cudaStream_t st);
     static cudaError_t from_f64(const double* in, T* out, size_t n, cudaStream_t st);
 };

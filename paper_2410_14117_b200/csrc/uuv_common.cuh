@@ -22,6 +22,11 @@
 #define __forceinline__ inline
 #endif
 
+#ifndef UUV_PACK_CONSTS
+#define UUV_PACK_CONSTS 0   // fp32 Fossen vehicle constants in registers (1) or constant bank (0):
+                            // bank operands keep FFMAs at 2 register reads (full issue rate)
+#endif
+
 namespace uuv {
 
 constexpr int MAX_THR = 8;
@@ -168,6 +173,11 @@ template <class T> struct EngineP {
     uint64_t* param_ctr;
     V4<T>* dr0; V4<T>* dr1; V2<T>* dr2;
     double* stats;         // [gridDim][NSTAT] per-block partials
+    // fp32 register pack per vehicle (PACK_F4 float4 each, see uuv_model.cuh
+    // load_regs): read once per step with LDG so ptxas keeps it in registers
+    const float4* vpack;
 };
+
+constexpr int PACK_F4 = 10;   // 40 floats: Fossen pattern + restoring + trig constants
 
 }  // namespace uuv

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "uuv_model.cuh"
 #include "launch.h"
@@ -22,38 +23,45 @@
 namespace uuv {
 
 
+// stored angles are wrapped; only a teacher-forced state can lie outside
+// [-pi, pi] -- bring it in once so every sub-step can use sincos_poly
+__device__ __forceinline__ void prewrap(float s[12]) {
+    if (!(fmaxf(fabsf(s[3]), fmaxf(fabsf(s[4]), fabsf(s[5]))) <= Consts<float>::PI)) {
+        s[3] = wrap_pi(s[3]);
+        s[4] = wrap_pi(s[4]);
+        s[5] = wrap_pi(s[5]);
+    }
+}
+
+template <bool DR, class Pat>
+__device__ __forceinline__ void replay_env(const EngineP<float>& p, const VehP<float>& V,
+                                        const EnvParams<float, DR || (UUV_PACK_CONSTS && Pat::fossen)>& E, int e,
+                                        const float tau[6], float dt, const TrigK& K, int n,
+                                        float s[12]) {
+    const V4<float> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
+    const float r[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+#pragma unroll
+    for (int i = 0; i < 12; ++i) s[i] = r[i];
+    prewrap(s);
+    for (int k = 0; k < n; ++k) substep_fused<DR, Pat>(V, E, s, tau, dt, K);
+}
+
+// Per-thread episode-statistics accumulator (one or two envs per thread).
+struct StatAcc {
+    float rew = 0.f, epret = 0.f;
+    int eplen = 0, n_tr = 0, n_dv = 0, n_fl = 0, n_act = 0, n_err = 0;
+};
+
+// Reward / termination / auto-reset / stores / observation for one env whose
+// sub-steps are done (tasks.py:219-230, batch.py:101-118, engine.rs:543-568).
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
-__device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
-                                         const T* __restrict__ act, T* __restrict__ obs,
-                                         T* __restrict__ rew, uint8_t* __restrict__ done,
-                                         int8_t* __restrict__ reason, float& st_rew,
-                                         int& st_reason, float& st_epret, int& st_eplen,
-                                         int& st_err) {
+__device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t g, T s[12],
+                                           int32_t step, bool failed, T* __restrict__ obs,
+                                           T* __restrict__ rew, uint8_t* __restrict__ done,
+                                           int8_t* __restrict__ reason, StatAcc& st) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
-    const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
-    T s[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
-    const int32_t step = p.step[e];
-
-    EnvParams<T, DR> E;
-    if constexpr (DR) {
-        const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
-        const V2<T> d2 = p.dr2[e];
-        build_env<T, Pat>(V, d0, d1, d2, E);
-    }
-    T tau[6];
-    wrench<T, DR>(V, E, act + (size_t)e * p.act_dim, tau);
-
-    bool failed = false;
-    const T dt = tk.sub_dt;
-#pragma unroll 2
-    for (int k = 0; k < tk.n_substeps; ++k) {
-        if (!substep<T, DR, Pat>(V, E, s, tau, dt)) {
-            failed = true;
-            break;
-        }
-    }
-    // reward / termination (tasks.py:219-230): failure > divergence > truncation
+    // reward / termination: failure > divergence > truncation
     const int32_t ns = step + 1;
     const int tab_last = tk.episode_len + tk.lookahead;
     T rx, ry, rz;
@@ -74,8 +82,8 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
     float er = p.ep_ret[e] + (float)reward;
     int32_t nstep = ns;
     if (rc >= 0) {
-        st_epret = er;
-        st_eplen = ns;
+        st.epret += er;
+        st.eplen += ns;
         er = 0.0f;
         const uint64_t seed = *p.seed_dev;
         if constexpr (DR) {
@@ -86,7 +94,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
                 if (dr_draw<T>(V, p.ranges, seed, g, pc, n0, n1, n2)) {
                     p.dr0[e] = n0; p.dr1[e] = n1; p.dr2[e] = n2;
                 } else {
-                    st_err = 1;
+                    st.n_err += 1;
                 }
                 p.param_ctr[e] = pc;
             }
@@ -132,29 +140,145 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
     rew[e] = reward;
     done[e] = rc >= 0 ? 1 : 0;
     if (reason) reason[e] = (int8_t)rc;
-    st_rew = (float)reward;
-    st_reason = rc;
+    st.rew += (float)reward;
+    st.n_act += 1;
+    st.n_tr += rc == 0;
+    st.n_dv += rc == 1;
+    st.n_fl += rc == 2;
 }
 
-// Block-level episode statistics: warp shuffles -> shared memory -> one
+template <class T>
+__device__ __forceinline__ void load_state(const EngineP<T>& p, int e, T s[12]) {
+    const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
+    s[0] = a0.x; s[1] = a0.y; s[2] = a0.z; s[3] = a0.w;
+    s[4] = a1.x; s[5] = a1.y; s[6] = a1.z; s[7] = a1.w;
+    s[8] = a2.x; s[9] = a2.y; s[10] = a2.z; s[11] = a2.w;
+}
+
+// One env per thread (every precision / pattern / randomisation mode).
+template <class T, bool TRACK, bool DR, int SLOT, class Pat>
+__device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
+                                         const T* __restrict__ act, T* __restrict__ obs,
+                                         T* __restrict__ rew, uint8_t* __restrict__ done,
+                                         int8_t* __restrict__ reason, StatAcc& st) {
+    const VehP<T>& V = p.veh[SLOT];
+    const TaskP<T>& tk = p.task;
+    T s[12];
+    load_state(p, e, s);
+    const int32_t step = p.step[e];
+    if constexpr (!is_f64<T>()) prewrap(s);
+
+    // fp32: Fossen-pattern parameters live in registers for the whole step
+    constexpr bool REG = DR || (UUV_PACK_CONSTS && !is_f64<T>() && Pat::fossen);
+    EnvParams<T, REG> E;
+    [[maybe_unused]] float dt32 = 0.0f;
+    [[maybe_unused]] TrigK K{};
+    if constexpr (!is_f64<T>()) {
+        RegPack R;
+        load_pack(p.vpack + SLOT * PACK_F4, R);
+        if constexpr (!DR && REG) load_regs<Pat>(R, E, dt32, K);
+        else load_trig(R, dt32, K);
+    }
+    if constexpr (DR) {
+        const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
+        const V2<T> d2 = p.dr2[e];
+        build_env<T, Pat>(V, d0, d1, d2, E);
+    }
+    T tau[6];
+    wrench<T, DR, REG>(V, E, act + (size_t)e * p.act_dim, tau);
+
+    bool failed = false;
+    if constexpr (is_f64<T>()) {
+        const T dt = tk.sub_dt;
+#pragma unroll 1
+        for (int k = 0; k < tk.n_substeps; ++k) {
+            if (!substep<T, DR, Pat>(V, E, s, tau, dt)) {
+                failed = true;
+                break;
+            }
+        }
+    } else {
+        // in-place sub-steps without an early exit; the first non-finite one is
+        // recorded and the env replayed from its initial state (still in HBM)
+        // up to the last finite sub-step
+        const float dt = dt32;
+        int fail_at = -1;
+#pragma unroll 1
+        for (int k = 0; k < tk.n_substeps; ++k) {
+            const bool ok = substep_fused<DR, Pat>(V, E, s, tau, dt, K);
+            fail_at = (!ok && fail_at < 0) ? k : fail_at;
+        }
+        if (fail_at >= 0) {
+            failed = true;
+            replay_env<DR, Pat>(p, V, E, e, tau, dt, K, fail_at, s);
+        }
+    }
+    finish_env<T, TRACK, DR, SLOT, Pat>(p, e, g, s, step, failed, obs, rew, done, reason, st);
+}
+
+// Two envs per thread sharing the register-resident vehicle constants (fp32,
+// Fossen pattern, no randomisation): two independent dependency chains per
+// thread hide latency at half the registers of two threads.
+template <bool TRACK, int SLOT>
+__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1,
+                                          const float* __restrict__ act, float* __restrict__ obs,
+                                          float* __restrict__ rew, uint8_t* __restrict__ done,
+                                          int8_t* __restrict__ reason, StatAcc& st) {
+    using Pat = PatFossen;
+    const VehP<float>& V = p.veh[SLOT];
+    const TaskP<float>& tk = p.task;
+    float s0[12], s1[12];
+    load_state(p, e0, s0);
+    load_state(p, e1, s1);
+    const int32_t step0 = p.step[e0], step1 = p.step[e1];
+    prewrap(s0);
+    prewrap(s1);
+    constexpr bool REG = UUV_PACK_CONSTS;
+    EnvParams<float, REG> E;
+    float dt;
+    TrigK K;
+    {
+        RegPack R;
+        load_pack(p.vpack + SLOT * PACK_F4, R);
+        if constexpr (REG && SLOT >= 0) load_regs<Pat>(R, E, dt, K);
+        else load_trig(R, dt, K);
+    }
+    float tau0[6], tau1[6];
+    wrench<float, false, REG>(V, E, act + (size_t)e0 * p.act_dim, tau0);
+    wrench<float, false, REG>(V, E, act + (size_t)e1 * p.act_dim, tau1);
+    int f0 = -1, f1 = -1;
+#pragma unroll 1
+    for (int k = 0; k < tk.n_substeps; ++k) {
+        const bool ok0 = substep_fused<false, Pat>(V, E, s0, tau0, dt, K);
+        const bool ok1 = substep_fused<false, Pat>(V, E, s1, tau1, dt, K);
+        f0 = (!ok0 && f0 < 0) ? k : f0;
+        f1 = (!ok1 && f1 < 0) ? k : f1;
+    }
+    if (f0 >= 0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, f0, s0);
+    if (f1 >= 0) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, f1, s1);
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, p.env_offset + (uint64_t)e0, s0, step0,
+                                               f0 >= 0, obs, rew, done, reason, st);
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, p.env_offset + (uint64_t)e1, s1, step1,
+                                               f1 >= 0, obs, rew, done, reason, st);
+}
+
+// Block-level episode statistics: warp reductions -> shared memory -> one
 // read-modify-write of this block's own partial slot (no atomics, deterministic).
-__device__ __forceinline__ void block_stats(double* __restrict__ part, bool active, float rew,
-                                            int reason, float epret, int eplen, int err) {
+__device__ __forceinline__ void block_stats(double* __restrict__ part, const StatAcc& st) {
     __shared__ double sh[BLOCK / 32][NSTAT];
     const unsigned full = 0xffffffffu;
-    float r = rew, er = epret;
-    int el = eplen;
+    float r = st.rew, er = st.epret;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         r += __shfl_xor_sync(full, r, o);
         er += __shfl_xor_sync(full, er, o);
-        el += __shfl_xor_sync(full, el, o);
     }
-    const int n_tr = __popc(__ballot_sync(full, reason == 0));
-    const int n_dv = __popc(__ballot_sync(full, reason == 1));
-    const int n_fl = __popc(__ballot_sync(full, reason == 2));
-    const int n_ac = __popc(__ballot_sync(full, active));
-    const int n_er = __popc(__ballot_sync(full, err != 0));
+    const int el = __reduce_add_sync(full, st.eplen);
+    const int n_tr = __reduce_add_sync(full, st.n_tr);
+    const int n_dv = __reduce_add_sync(full, st.n_dv);
+    const int n_fl = __reduce_add_sync(full, st.n_fl);
+    const int n_ac = __reduce_add_sync(full, st.n_act);
+    const int n_er = __reduce_add_sync(full, st.n_err);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) {
         sh[w][ST_REWARD] = r;
@@ -176,25 +300,47 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, bool acti
 }
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
-__global__ void __launch_bounds__(BLOCK)
+__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, const T* act, T* obs,
+                                        T* rew, uint8_t* done, int8_t* reason, StatAcc& st) {
+    const uint64_t g = p.env_offset + (uint64_t)e;
+    bool slot1 = false;
+    if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
+    if (!slot1)
+        step_env<T, TRACK, DR, 0, Pat>(p, e, g, act, obs, rew, done, reason, st);
+    else if constexpr (MIX)
+        step_env<T, TRACK, DR, 1, Pat>(p, e, g, act, obs, rew, done, reason, st);
+}
+
+template <class T, bool TRACK, bool DR, bool MIX, class Pat>
+__global__ void __launch_bounds__(BLOCK, DR ? STEP_MIN_BLOCKS_DR : STEP_MIN_BLOCKS)
 k_step(const __grid_constant__ EngineP<T> p, const T* __restrict__ act, T* __restrict__ obs,
        T* __restrict__ rew, uint8_t* __restrict__ done, int8_t* __restrict__ reason) {
     const int e = blockIdx.x * BLOCK + threadIdx.x;
-    const bool active = e < p.n_env;
-    float st_rew = 0.f, st_epret = 0.f;
-    int st_reason = -1, st_eplen = 0, st_err = 0;
-    if (active) {
-        const uint64_t g = p.env_offset + (uint64_t)e;
-        bool slot1 = false;
-        if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
-        if (!slot1)
-            step_env<T, TRACK, DR, 0, Pat>(p, e, g, act, obs, rew, done, reason, st_rew,
-                                          st_reason, st_epret, st_eplen, st_err);
-        else if constexpr (MIX)
-            step_env<T, TRACK, DR, 1, Pat>(p, e, g, act, obs, rew, done, reason, st_rew,
-                                          st_reason, st_epret, st_eplen, st_err);
+    StatAcc st;
+    if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason, st);
+    if (p.stats_on) block_stats(p.stats, st);
+}
+
+// Paired variant: block b covers envs [2*BLOCK*b, 2*BLOCK*(b+1)); thread t
+// steps envs t and t+BLOCK of that span (both loads stay coalesced).
+template <bool TRACK, bool MIX>
+__global__ void __launch_bounds__(BLOCK, PAIR_MIN_BLOCKS)
+k_step_pair(const __grid_constant__ EngineP<float> p, const float* __restrict__ act,
+            float* __restrict__ obs, float* __restrict__ rew, uint8_t* __restrict__ done,
+            int8_t* __restrict__ reason) {
+    const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
+    StatAcc st;
+    const bool a0 = e0 < p.n_env, a1 = e1 < p.n_env;
+    const int sl0 = MIX && (int64_t)(p.env_offset + (uint64_t)e0) >= p.mix_bound0;
+    const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
+    if (a0 && a1 && sl0 == sl1) {
+        if (sl0 == 0) step_pair<TRACK, 0>(p, e0, e1, act, obs, rew, done, reason, st);
+        else if constexpr (MIX) step_pair<TRACK, 1>(p, e0, e1, act, obs, rew, done, reason, st);
+    } else {
+        if (a0) one_env<float, TRACK, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason, st);
+        if (a1) one_env<float, TRACK, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason, st);
     }
-    if (p.stats_on) block_stats(p.stats, active, st_rew, st_reason, st_epret, st_eplen, st_err);
+    if (p.stats_on) block_stats(p.stats, st);
 }
 
 // observation of the current state at the current step (reset / inspection)
@@ -309,10 +455,21 @@ __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restri
 
 // ------------------------------------------------------------------ launchers
 template <class T>
-cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, const T* act,
-                            T* obs, T* rew, uint8_t* done, int8_t* reason, cudaStream_t st) {
-    const dim3 grid((p.n_env + BLOCK - 1) / BLOCK);
+cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
+                            const T* act, T* obs, T* rew, uint8_t* done, int8_t* reason,
+                            cudaStream_t st) {
     const bool mix = p.n_veh > 1;
+    if constexpr (std::is_same<T, float>::value) {
+        if (pair && fossen && !dr) {
+            const dim3 grid((p.n_env + 2 * BLOCK - 1) / (2 * BLOCK));
+#define UUV_P(TR, M) k_step_pair<TR, M><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
+            if (track) { if (mix) UUV_P(true, true); else UUV_P(true, false); }
+            else { if (mix) UUV_P(false, true); else UUV_P(false, false); }
+#undef UUV_P
+            return cudaGetLastError();
+        }
+    }
+    const dim3 grid((p.n_env + BLOCK - 1) / BLOCK);
 #define UUV_L(TR, D, M, PAT) \
     k_step<T, TR, D, M, PAT><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
 #define UUV_LP(TR, D, M) \
@@ -367,7 +524,15 @@ cudaError_t Launch<T>::pack_dr(const EngineP<T>& p, double* out, cudaStream_t st
 
 template <class T>
 cudaError_t Launch<T>::step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
-                                  bool mix) {
+                                  bool mix, bool pair) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (pair && fossen && !dr) {
+            if (track) return mix ? cudaFuncGetAttributes(a, k_step_pair<true, true>)
+                                  : cudaFuncGetAttributes(a, k_step_pair<true, false>);
+            return mix ? cudaFuncGetAttributes(a, k_step_pair<false, true>)
+                       : cudaFuncGetAttributes(a, k_step_pair<false, false>);
+        }
+    }
 #define UUV_A(TR, D, M, PAT) return cudaFuncGetAttributes(a, k_step<T, TR, D, M, PAT>)
 #define UUV_AP(TR, D, M) \
     if (fossen) UUV_A(TR, D, M, PatFossen); else UUV_A(TR, D, M, PatDense)

@@ -48,8 +48,9 @@ def teacher_forced(cfg, steps=36):
         live = ~dr & ~band
         err = P.abs_err(sg[live], sr[live], P.STATE_ANGLES)
         scaled = err / (P.ABS_TOL + P.REL_TOL * np.abs(sr[live]))
-        worst = np.maximum(worst, err.max(axis=0))
-        worst_scaled = np.maximum(worst_scaled, scaled.max(axis=0))
+        if err.size:
+            worst = np.maximum(worst, err.max(axis=0))
+            worst_scaled = np.maximum(worst_scaled, scaled.max(axis=0))
         idx = np.argwhere(scaled > 1.0)
         for e_, c_ in idx[:20]:
             env = np.flatnonzero(live)[e_]
