@@ -332,6 +332,13 @@ void Engine::parse(const std::string& text) {
         cudaGetDevice(&device_);
     }
 
+    // engine.rs:258 -- M_RB + M_A must be positive definite (checked before any device work)
+    for (const BaseVehicle& v : veh_) {
+        double m_rb[36], m_total[36], L[36];
+        mass_matrices(v, m_rb, m_total);
+        if (!cholesky6(m_total, L))
+            throw ConfigError("M_RB + M_A is not positive definite: matrix is not positive definite");
+    }
     obs_dim_ = task_.kind == 0 ? 12 : 6 * task_.lookahead + 6;
     n_act_ = 0;
     for (auto& v : veh_) n_act_ = std::max<int>(n_act_, (int)v.kmax.size());

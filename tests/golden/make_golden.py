@@ -217,6 +217,20 @@ def main():
     np.savez_compressed(HERE / "traces.npz", **traces)
     (HERE / "kat.json").write_text(json.dumps(kats(), indent=1) + "\n")
     (HERE / "vehicles.json").write_text(json.dumps({"bluerov2_heavy": HEAVY}, indent=1) + "\n")
+    # engine-config documents the reference renders for its native engine
+    ecs = []
+    for task_in, rnd_in, n, seed in (
+            ({"kind": "station_keeping", "target": [1.0, -2.0, 3.0, 0.1, -0.2, 7.0]}, None, 8, 3),
+            ({"kind": "lemniscate", "lookahead": 3, "episode_len": 99, "scale": 2.5},
+             dict(DR_EP), 64, 2**63 + 5),
+            ({"kind": "helix", "center": [1.5, -0.5], "radius": 2.0, "climb_rate": 0.1,
+              "control_dt": 0.04, "n_substeps": 8}, {"mass": [0.8, 1.2]}, 5, 0)):
+        veh = VehicleParams.from_dict(HEAVY)
+        task = rconfig.task_from_dict(task_in)
+        ranges = RandomizationRanges.from_dict(rnd_in) if rnd_in is not None else None
+        ecs.append({"task_in": task_in, "randomization_in": rnd_in, "num_envs": n, "seed": seed,
+                    "engine_config": rconfig.engine_config_dict(veh, task, n, seed, 0, ranges)})
+    (HERE / "engine_configs.json").write_text(json.dumps(ecs, indent=1) + "\n")
     print("wrote", HERE)
 
 

@@ -1,0 +1,150 @@
+"""C-ABI boundary tests that need no GPU: exports, versioning, misuse, config errors.
+
+Mirrors the reference's ABI contract (reference pkg/native/src/capi.rs:1-253,
+SPEC.md:540-563): every documented misuse returns an error code with a
+retrievable thread-local message and never crashes; config problems are code 1
+with the reference engine's own messages (engine.rs:174-229, 350-417).
+"""
+
+from __future__ import annotations
+
+import copy
+import ctypes
+import importlib
+import json
+import os
+import re
+import sys
+from pathlib import Path
+
+import pytest
+
+import paper_2410_14117_b200 as uuv
+from paper_2410_14117_b200 import _core
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "uuvsim.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2410_14117_b200 import build
+    build.build()
+    return _core.load()
+
+
+def _declared_symbols():
+    return sorted(set(re.findall(r"\b(uuvsim_\w+)\s*\(", HEADER.read_text())))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    syms = _declared_symbols()
+    assert len(syms) >= 25
+    for name in syms:
+        assert hasattr(lib, name), name
+    # the ten ABI-v1 symbols the reference binds (reference _native.py:49-78)
+    for name in _core.SYMBOLS:
+        assert name in syms
+
+
+def test_abi_version(lib):
+    assert lib.uuvsim_abi_version() == 1
+
+
+def _err(lib):
+    return _core.last_error(lib)
+
+
+def test_invalid_handle_paths(lib):
+    spec = (ctypes.c_uint64 * 4)()
+    assert lib.uuvsim_spec(987654321, spec) == 2
+    assert "not valid" in _err(lib)
+    assert lib.uuvsim_destroy(987654321) == 2
+    buf = (ctypes.c_double * 4)()
+    assert lib.uuvsim_states(987654321, buf, 4) == 2
+    assert lib.uuvsim_set_threads(987654321, 0) == 2
+    assert lib.uuvsim_step(987654321, None, 0, None, 0, None, 0, None, 0) == 2
+
+
+def test_last_error_contract(lib):
+    lib.uuvsim_destroy(424242)
+    full = _core.last_error(lib)
+    small = ctypes.create_string_buffer(5)
+    n = lib.uuvsim_last_error(small, 5)
+    assert n == len(full) > 5                    # full length returned
+    assert small.raw[:5] == full.encode()[:5]    # min(len, cap) bytes copied
+    assert lib.uuvsim_last_error(None, 0) == len(full)
+
+
+def _create(lib, cfg):
+    h = ctypes.c_uint64(0)
+    text = cfg if isinstance(cfg, str) else json.dumps(cfg)
+    return lib.uuvsim_create(text.encode(), ctypes.byref(h)), _err(lib)
+
+
+BASE = uuv.engine_config_dict(uuv.default_params(), uuv.TaskSpec(), 16, 0)
+
+
+@pytest.mark.parametrize("mutate,needle", [
+    (lambda c: c.pop("seed"), "seed"),
+    (lambda c: c.pop("vehicle"), "config must include 'vehicle' or 'vehicle_params'"),
+    (lambda c: c["task"].__setitem__("kind", "spiral"), 'unknown task kind "spiral"'),
+    (lambda c: c["task"].__setitem__("n_substeps", 0), "invalid task timing settings"),
+    (lambda c: c["task"].__setitem__("control_dt", -0.1), "invalid task timing settings"),
+    (lambda c: c["task"].update(kind="circle", radius=0.0), "radius must be positive"),
+    (lambda c: c["task"].update(kind="lemniscate", scale=-1.0), "scale must be positive"),
+    (lambda c: c["batch"].__setitem__("num_envs", 0), "batch.num_envs must be >= 1"),
+    (lambda c: c["batch"].__setitem__("randomization", {"mass": [1.2, 1.1]}),
+     "range mass must satisfy 0 < lo <= hi"),
+    (lambda c: c["batch"].__setitem__("randomization", {"rb_offset": -1.0}),
+     "rb_offset must be >= 0"),
+    (lambda c: c["vehicle"].__setitem__("mass", 0.0), "mass must be positive"),
+    (lambda c: c["vehicle"].__setitem__("buoyancy", -1.0), "weight and buoyancy must be >= 0"),
+    (lambda c: c["vehicle"].__setitem__("thrusters", []), "layout needs at least one thruster"),
+    (lambda c: c["vehicle"]["thrusters"][0].__setitem__("direction", [1.0, 1.0, 0.0]),
+     "thruster direction must be unit norm"),
+    (lambda c: c["vehicle"]["thrusters"][0].__setitem__("curve", "cubic"),
+     'unknown thrust curve "cubic"'),
+    (lambda c: c["vehicle"]["damping_quadratic"].__setitem__(2, -1.0),
+     "damping_quadratic components must be >= 0"),
+    (lambda c: c["vehicle"].__setitem__("inertia", [[1.0, 0.0], [0.0, 1.0]]), "inertia must be 3x3"),
+    (lambda c: c["vehicle"].__setitem__("added_mass",
+                                        [[-100.0 if i == j == 0 else 0.0 for j in range(6)]
+                                         for i in range(6)]),
+     "M_RB + M_A is not positive definite"),
+    (lambda c: c["device"].__setitem__("precision", "fp16"), "device.precision"),
+    (lambda c: c.update(vehicles=[c["vehicle"], c["vehicle"]]), "vehicle_mix"),
+])
+def test_config_errors_are_code_1(lib, mutate, needle):
+    cfg = copy.deepcopy(BASE)
+    mutate(cfg)
+    code, msg = _create(lib, cfg)
+    assert code == 1, (code, msg)
+    assert needle in msg
+
+
+def test_malformed_json_and_null_pointer(lib):
+    code, msg = _create(lib, "{not json")
+    assert code == 1 and "not valid JSON" in msg
+    h = ctypes.c_uint64()
+    assert lib.uuvsim_create(None, ctypes.byref(h)) == 1
+
+
+def test_reference_binding_loads_this_library(lib, monkeypatch):
+    """Drop-in: the reference's own ctypes loader binds libuuvsim_core.so (ABI v1).
+
+    Runs only where the reference tree is mounted (the build container); the
+    GPU-box equivalent is the reference-shaped binding in _core.py."""
+    ref = Path("/root/reference/pkg/src")
+    if not ref.is_dir():
+        pytest.skip("reference tree not present")
+    monkeypatch.setenv("UUVSIM_CORE_LIB", str(_core.lib_path()))
+    monkeypatch.syspath_prepend(str(ref))
+    for m in [m for m in sys.modules if m == "uuvsim" or m.startswith("uuvsim.")]:
+        monkeypatch.delitem(sys.modules, m)
+    native = importlib.import_module("uuvsim._native")
+    L = native.load_native_lib()
+    assert L is not None and L.uuvsim_abi_version() == 1
+    assert native.native_available()
+    batch = importlib.import_module("uuvsim.batch")
+    assert batch.resolve_backend() == "native"
