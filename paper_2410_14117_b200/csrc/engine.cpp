@@ -433,6 +433,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.stats_on = stats_on_ ? 1 : 0;
     p.stats = stats_part_;
     p.vpack = d_vpack_;
+    p.io_f64 = fp64_ ? 1 : 0;   // device face: engine precision; host ABI: set per launch
 
     // device buffers carved from the arena
     char* a = static_cast<char*>(arena_);
@@ -591,6 +592,8 @@ Engine::~Engine() { release(); }
 void Engine::release() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     graph_exec_ = nullptr;
+    if (abi_graph_.exec) cudaGraphExecDestroy(abi_graph_.exec);
+    abi_graph_ = AbiGraph{};
     if (!fp64_) {
         void* t[] = {d_actT_, d_obsT_, d_rewT_};
         for (void* b : t)
@@ -646,25 +649,72 @@ void Engine::reset_host(uint64_t seed, double* obs) {
     else reset_host_T<float>(seed, obs);
 }
 
-// uuvsim_step: H2D actions -> (convert) -> fused step -> (convert) -> D2H outputs
+// uuvsim_step: H2D f64 actions -> one fused step reading f64 actions and writing
+// f64 obs/reward directly (io_f64) -> D2H outputs
 template <class T>
-void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* done,
-                         int8_t* reason) {
+void Engine::enqueue_step_host(const double* act, double* obs, double* rew, uint8_t* done,
+                               int8_t* reason) {
     const size_t N = (size_t)m_, n_act = N * n_act_, n_obs = N * obs_dim_;
     cuda_check(cudaMemcpyAsync(d_act64_, act, n_act * 8, cudaMemcpyHostToDevice, stream_),
                "step H2D");
-    if (!fp64_) cuda_check(Launch<T>::from_f64(d_act64_, (T*)d_actT_, n_act, stream_), "act cvt");
-    cuda_check(Launch<T>::step(P<T>(), task_.kind != 0, ranges_.enabled, fossen_, pair_, (T*)d_actT_,
-                               (T*)d_obsT_, (T*)d_rewT_, d_done_, d_reason_, stream_), "step");
-    if (!fp64_) {
-        cuda_check(Launch<T>::to_f64((T*)d_obsT_, d_obs64_, n_obs, stream_), "obs cvt");
-        cuda_check(Launch<T>::to_f64((T*)d_rewT_, d_rew64_, N, stream_), "rew cvt");
-    }
+    EngineP<T>& p = P<T>();
+    p.io_f64 = 1;
+    const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
+                                          d_act64_, d_obs64_, d_rew64_, d_done_, d_reason_,
+                                          stream_);
+    p.io_f64 = fp64_ ? 1 : 0;
+    cuda_check(e, "step");
     cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
     cuda_check(cudaMemcpyAsync(rew, d_rew64_, N * 8, cudaMemcpyDeviceToHost, stream_), "rew D2H");
     cuda_check(cudaMemcpyAsync(done, d_done_, N, cudaMemcpyDeviceToHost, stream_), "done D2H");
     if (reason)
         cuda_check(cudaMemcpyAsync(reason, d_reason_, N, cudaMemcpyDeviceToHost, stream_), "reason D2H");
+}
+
+namespace {
+bool page_locked(const void* ptr) {
+    if (!ptr) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+template <class T>
+void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* done,
+                         int8_t* reason) {
+    AbiGraph& g = abi_graph_;
+    const bool same = g.exec && g.act == act && g.obs == obs && g.rew == rew && g.done == done &&
+                      g.reason == reason;
+    if (!same && page_locked(act) && page_locked(obs) && page_locked(rew) && page_locked(done) &&
+        page_locked(reason)) {
+        // (re)capture the whole host-ABI step for these page-locked buffers
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = AbiGraph{};
+        cuda_check(cudaStreamSynchronize(stream_), "abi capture pre-sync");
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "abi capture");
+        try {
+            enqueue_step_host<T>(act, obs, rew, done, reason);
+        } catch (...) {
+            cudaStreamEndCapture(stream_, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(stream_, &graph), "abi capture end");
+        const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(e, "abi graph instantiate");
+        g.act = act; g.obs = obs; g.rew = rew; g.done = done; g.reason = reason;
+    }
+    if (g.exec && g.act == act && g.obs == obs && g.rew == rew && g.done == done &&
+        g.reason == reason)
+        cuda_check(cudaGraphLaunch(g.exec, stream_), "abi graph launch");
+    else
+        enqueue_step_host<T>(act, obs, rew, done, reason);   // pageable buffers
     cuda_check(cudaStreamSynchronize(stream_), "step sync");
 }
 

@@ -152,6 +152,18 @@ private:
     float4* d_vpack_ = nullptr;
     cudaStream_t stream_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
+    // host-ABI step replayed as one CUDA graph (H2D -> step -> D2H) while the
+    // caller keeps passing the same page-locked buffers
+    struct AbiGraph {
+        const void* act = nullptr;
+        void* obs = nullptr;
+        void* rew = nullptr;
+        void* done = nullptr;
+        void* reason = nullptr;
+        cudaGraphExec_t exec = nullptr;
+    } abi_graph_;
+    template <class T> void enqueue_step_host(const double* act, double* obs, double* rew,
+                                              uint8_t* done, int8_t* reason);
     std::string device_name_;
     int sm_count_ = 0;
 };

@@ -31,9 +31,10 @@ constexpr long PAIR_AUTO_MIN_ENVS = UUV_PAIR_AUTO_MIN_ENVS;
 template <class T> struct Launch {
     // one fused step; fossen selects the structure-specialised variant, pair the
     // two-envs-per-thread kernel (fp32, Fossen, no randomisation)
+    // act/obs/rew element type: T, or double when p.io_f64 (host-ABI path)
     static cudaError_t step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
-                            const T* act, T* obs, T* rew, uint8_t* done, int8_t* reason,
-                            cudaStream_t st);
+                            const void* act, void* obs, void* rew, uint8_t* done,
+                            int8_t* reason, cudaStream_t st);
     static cudaError_t reset(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t observe(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);

@@ -165,6 +165,8 @@ template <class T> struct EngineP {
     int32_t n_veh;
     int32_t act_dim;       // row stride of the action matrix
     int32_t stats_on;
+    int32_t io_f64;        // actions / obs / reward are f64 (host ABI path), else T
+    int32_t pad_io;
     // device buffers
     V4<T>* s0; V4<T>* s1; V4<T>* s2;
     int32_t* step;

@@ -54,19 +54,94 @@ struct StatAcc {
 
 // Reward / termination / auto-reset / stores / observation for one env whose
 // sub-steps are done (tasks.py:219-230, batch.py:101-118, engine.rs:543-568).
+// Everything one env reads from HBM, issued together in the prologue so a
+// cold-cache step pays one memory round trip instead of several serialised ones
+// (state, step counter, running return, actions, DR record, and -- tracking --
+// the LA_PRE+1 trajectory rows the reward and observation will need).
+constexpr int LA_PRE = 5;
+
+template <class T, bool TRACK> struct EnvIn {
+    T s[12];
+    int32_t step;
+    float ep_ret;
+    V4<T> rows[TRACK ? LA_PRE + 1 : 1];   // traj[step+1 .. step+1+LA_PRE]
+};
+
+template <class T, bool TRACK>
+__device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TRACK>& in) {
+    const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
+    in.s[0] = a0.x; in.s[1] = a0.y; in.s[2] = a0.z; in.s[3] = a0.w;
+    in.s[4] = a1.x; in.s[5] = a1.y; in.s[6] = a1.z; in.s[7] = a1.w;
+    in.s[8] = a2.x; in.s[9] = a2.y; in.s[10] = a2.z; in.s[11] = a2.w;
+    in.step = p.step[e];
+    in.ep_ret = p.ep_ret[e];
+    if constexpr (TRACK) {
+        const int tab_last = p.task.episode_len + p.task.lookahead;
+#pragma unroll
+        for (int k = 0; k <= LA_PRE; ++k)
+            in.rows[k] = p.task.traj[min(max(in.step + 1 + k, 0), tab_last)];
+    }
+}
+
+// observation row of one env (post-reset for finished envs, batch.py:106-118),
+// stored as O = T (device face) or double (host ABI)
+template <class T, class O, bool TRACK>
+__device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ row, const T s[12],
+                                          const EnvIn<T, TRACK>& in, int32_t nstep, bool pre) {
+    if constexpr (!TRACK) {
+        V4<O>* o4 = reinterpret_cast<V4<O>*>(row);
+        o4[0] = V4<O>{(O)(tk.target[0] - s[0]), (O)(tk.target[1] - s[1]),
+                      (O)(tk.target[2] - s[2]), (O)obs_wrap<T>(tk.target[3] - s[3])};
+        o4[1] = V4<O>{(O)obs_wrap<T>(tk.target[4] - s[4]), (O)obs_wrap<T>(tk.target[5] - s[5]),
+                      (O)s[6], (O)s[7]};
+        o4[2] = V4<O>{(O)s[8], (O)s[9], (O)s[10], (O)s[11]};
+    } else {
+        const int tab_last = tk.episode_len + tk.lookahead;
+        V2<O>* o2 = reinterpret_cast<V2<O>*>(row);
+        const O ephi = (O)obs_wrap<T>(T(0) - s[3]);
+        const O eth = (O)obs_wrap<T>(T(0) - s[4]);
+        if (pre) {   // trajectory rows prefetched by load_env
+#pragma unroll
+            for (int k = 1; k <= LA_PRE; ++k) {
+                if (k > tk.lookahead) break;
+                const V4<T> r = in.rows[k];
+                V2<O>* q = o2 + 3 * (k - 1);
+                q[0] = V2<O>{(O)(r.x - s[0]), (O)(r.y - s[1])};
+                q[1] = V2<O>{(O)(r.z - s[2]), ephi};
+                q[2] = V2<O>{eth, (O)obs_wrap<T>(r.w - s[5])};
+            }
+        } else {
+#pragma unroll 1
+            for (int k = 1; k <= tk.lookahead; ++k) {
+                const V4<T> r = tk.traj[min(nstep + k, tab_last)];
+                V2<O>* q = o2 + 3 * (k - 1);
+                q[0] = V2<O>{(O)(r.x - s[0]), (O)(r.y - s[1])};
+                q[1] = V2<O>{(O)(r.z - s[2]), ephi};
+                q[2] = V2<O>{eth, (O)obs_wrap<T>(r.w - s[5])};
+            }
+        }
+        V2<O>* q = o2 + 3 * tk.lookahead;
+        q[0] = V2<O>{(O)s[6], (O)s[7]};
+        q[1] = V2<O>{(O)s[8], (O)s[9]};
+        q[2] = V2<O>{(O)s[10], (O)s[11]};
+    }
+}
+
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
 __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t g, T s[12],
-                                           int32_t step, bool failed, T* __restrict__ obs,
-                                           T* __restrict__ rew, uint8_t* __restrict__ done,
+                                           const EnvIn<T, TRACK>& in, bool failed,
+                                           void* __restrict__ obs, void* __restrict__ rew,
+                                           uint8_t* __restrict__ done,
                                            int8_t* __restrict__ reason, StatAcc& st) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
+    const int32_t step = in.step;
     // reward / termination: failure > divergence > truncation
     const int32_t ns = step + 1;
     const int tab_last = tk.episode_len + tk.lookahead;
     T rx, ry, rz;
     if constexpr (TRACK) {
-        const V4<T> r = tk.traj[min(max(ns, 0), tab_last)];
+        const V4<T> r = in.rows[0];
         rx = r.x; ry = r.y; rz = r.z;
     } else {
         rx = tk.target[0]; ry = tk.target[1]; rz = tk.target[2];
@@ -79,7 +154,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t 
     else if (pe > tk.div_radius) rc = 1;
     else if (ns >= tk.episode_len) rc = 0;
 
-    float er = p.ep_ret[e] + (float)reward;
+    float er = in.ep_ret + (float)reward;
     int32_t nstep = ns;
     if (rc >= 0) {
         st.epret += er;
@@ -113,31 +188,14 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t 
     p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
 
     // observation (post-reset for finished envs, batch.py:106-118)
-    T* row = obs + (size_t)e * tk.obs_dim;
-    if constexpr (!TRACK) {
-        V4<T>* o4 = reinterpret_cast<V4<T>*>(row);
-        o4[0] = V4<T>{tk.target[0] - s[0], tk.target[1] - s[1], tk.target[2] - s[2],
-                      obs_wrap<T>(tk.target[3] - s[3])};
-        o4[1] = V4<T>{obs_wrap<T>(tk.target[4] - s[4]), obs_wrap<T>(tk.target[5] - s[5]), s[6], s[7]};
-        o4[2] = V4<T>{s[8], s[9], s[10], s[11]};
+    const bool pre = rc < 0 && tk.lookahead <= LA_PRE;
+    if (p.io_f64) {
+        write_obs<T, double, TRACK>(tk, (double*)obs + (size_t)e * tk.obs_dim, s, in, nstep, pre);
+        ((double*)rew)[e] = (double)reward;
     } else {
-        V2<T>* o2 = reinterpret_cast<V2<T>*>(row);
-        const T ephi = obs_wrap<T>(T(0) - s[3]);
-        const T eth = obs_wrap<T>(T(0) - s[4]);
-#pragma unroll 1
-        for (int k = 1; k <= tk.lookahead; ++k) {
-            const V4<T> r = tk.traj[min(nstep + k, tab_last)];
-            V2<T>* q = o2 + 3 * (k - 1);
-            q[0] = V2<T>{r.x - s[0], r.y - s[1]};
-            q[1] = V2<T>{r.z - s[2], ephi};
-            q[2] = V2<T>{eth, obs_wrap<T>(r.w - s[5])};
-        }
-        V2<T>* q = o2 + 3 * tk.lookahead;
-        q[0] = V2<T>{s[6], s[7]};
-        q[1] = V2<T>{s[8], s[9]};
-        q[2] = V2<T>{s[10], s[11]};
+        write_obs<T, T, TRACK>(tk, (T*)obs + (size_t)e * tk.obs_dim, s, in, nstep, pre);
+        ((T*)rew)[e] = reward;
     }
-    rew[e] = reward;
     done[e] = rc >= 0 ? 1 : 0;
     if (reason) reason[e] = (int8_t)rc;
     st.rew += (float)reward;
@@ -145,6 +203,13 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t 
     st.n_tr += rc == 0;
     st.n_dv += rc == 1;
     st.n_fl += rc == 2;
+}
+
+// start of env e's action row (elements are T, or f64 on the host-ABI path)
+template <class T>
+__device__ __forceinline__ const void* act_row(const EngineP<T>& p, const void* act, int e) {
+    return p.io_f64 ? (const void*)((const double*)act + (size_t)e * p.act_dim)
+                    : (const void*)((const T*)act + (size_t)e * p.act_dim);
 }
 
 template <class T>
@@ -158,26 +223,26 @@ __device__ __forceinline__ void load_state(const EngineP<T>& p, int e, T s[12]) 
 // One env per thread (every precision / pattern / randomisation mode).
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
 __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
-                                         const T* __restrict__ act, T* __restrict__ obs,
-                                         T* __restrict__ rew, uint8_t* __restrict__ done,
+                                         const void* __restrict__ act, void* __restrict__ obs,
+                                         void* __restrict__ rew, uint8_t* __restrict__ done,
                                          int8_t* __restrict__ reason, StatAcc& st) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
-    T s[12];
-    load_state(p, e, s);
-    const int32_t step = p.step[e];
+    EnvIn<T, TRACK> in;
+    load_env<T, TRACK>(p, e, in);
+    T* s = in.s;
     if constexpr (!is_f64<T>()) prewrap(s);
 
-    // fp32: Fossen-pattern parameters live in registers for the whole step
+    // fp32: Fossen-pattern parameters in registers (UUV_PACK_CONSTS) or in the
+    // constant bank (default: keeps FFMAs at two register reads)
     constexpr bool REG = DR || (UUV_PACK_CONSTS && !is_f64<T>() && Pat::fossen);
     EnvParams<T, REG> E;
-    [[maybe_unused]] float dt32 = 0.0f;
-    [[maybe_unused]] TrigK K{};
-    if constexpr (!is_f64<T>()) {
+    [[maybe_unused]] float dt32 = (float)tk.sub_dt;
+    [[maybe_unused]] TrigK K = TrigK::imm();
+    if constexpr (!is_f64<T>() && !DR && REG) {
         RegPack R;
         load_pack(p.vpack + SLOT * PACK_F4, R);
-        if constexpr (!DR && REG) load_regs<Pat>(R, E, dt32, K);
-        else load_trig(R, dt32, K);
+        load_regs<Pat>(R, E, dt32, K);
     }
     if constexpr (DR) {
         const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
@@ -185,7 +250,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
         build_env<T, Pat>(V, d0, d1, d2, E);
     }
     T tau[6];
-    wrench<T, DR, REG>(V, E, act + (size_t)e * p.act_dim, tau);
+    wrench<T, DR, REG>(V, E, act_row(p, act, e), p.io_f64, tau);
 
     bool failed = false;
     if constexpr (is_f64<T>()) {
@@ -213,7 +278,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
             replay_env<DR, Pat>(p, V, E, e, tau, dt, K, fail_at, s);
         }
     }
-    finish_env<T, TRACK, DR, SLOT, Pat>(p, e, g, s, step, failed, obs, rew, done, reason, st);
+    finish_env<T, TRACK, DR, SLOT, Pat>(p, e, g, s, in, failed, obs, rew, done, reason, st);
 }
 
 // Two envs per thread sharing the register-resident vehicle constants (fp32,
@@ -221,31 +286,31 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
 // thread hide latency at half the registers of two threads.
 template <bool TRACK, int SLOT>
 __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1,
-                                          const float* __restrict__ act, float* __restrict__ obs,
-                                          float* __restrict__ rew, uint8_t* __restrict__ done,
+                                          const void* __restrict__ act, void* __restrict__ obs,
+                                          void* __restrict__ rew, uint8_t* __restrict__ done,
                                           int8_t* __restrict__ reason, StatAcc& st) {
     using Pat = PatFossen;
     const VehP<float>& V = p.veh[SLOT];
     const TaskP<float>& tk = p.task;
-    float s0[12], s1[12];
-    load_state(p, e0, s0);
-    load_state(p, e1, s1);
-    const int32_t step0 = p.step[e0], step1 = p.step[e1];
+    EnvIn<float, TRACK> in0, in1;
+    load_env<float, TRACK>(p, e0, in0);
+    load_env<float, TRACK>(p, e1, in1);
+    float* s0 = in0.s;
+    float* s1 = in1.s;
     prewrap(s0);
     prewrap(s1);
     constexpr bool REG = UUV_PACK_CONSTS;
     EnvParams<float, REG> E;
-    float dt;
-    TrigK K;
-    {
+    float dt = tk.sub_dt;
+    TrigK K = TrigK::imm();
+    if constexpr (REG && SLOT >= 0) {
         RegPack R;
         load_pack(p.vpack + SLOT * PACK_F4, R);
-        if constexpr (REG && SLOT >= 0) load_regs<Pat>(R, E, dt, K);
-        else load_trig(R, dt, K);
+        load_regs<Pat>(R, E, dt, K);
     }
     float tau0[6], tau1[6];
-    wrench<float, false, REG>(V, E, act + (size_t)e0 * p.act_dim, tau0);
-    wrench<float, false, REG>(V, E, act + (size_t)e1 * p.act_dim, tau1);
+    wrench<float, false, REG>(V, E, act_row(p, act, e0), p.io_f64, tau0);
+    wrench<float, false, REG>(V, E, act_row(p, act, e1), p.io_f64, tau1);
     int f0 = -1, f1 = -1;
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
@@ -256,9 +321,9 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
     }
     if (f0 >= 0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, f0, s0);
     if (f1 >= 0) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, f1, s1);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, p.env_offset + (uint64_t)e0, s0, step0,
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, p.env_offset + (uint64_t)e0, s0, in0,
                                                f0 >= 0, obs, rew, done, reason, st);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, p.env_offset + (uint64_t)e1, s1, step1,
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, p.env_offset + (uint64_t)e1, s1, in1,
                                                f1 >= 0, obs, rew, done, reason, st);
 }
 
@@ -295,13 +360,15 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
         double acc = 0.0;
 #pragma unroll
         for (int i = 0; i < BLOCK / 32; ++i) acc += sh[i][threadIdx.x];
-        part[(size_t)blockIdx.x * NSTAT + threadIdx.x] += acc;
+        // RED (no return): one update per slot per step, steps are stream-ordered,
+        // so the accumulation order -- and the sum -- is deterministic
+        atomicAdd(&part[(size_t)blockIdx.x * NSTAT + threadIdx.x], acc);
     }
 }
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
-__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, const T* act, T* obs,
-                                        T* rew, uint8_t* done, int8_t* reason, StatAcc& st) {
+__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, const void* act, void* obs,
+                                        void* rew, uint8_t* done, int8_t* reason, StatAcc& st) {
     const uint64_t g = p.env_offset + (uint64_t)e;
     bool slot1 = false;
     if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
@@ -313,8 +380,9 @@ __device__ __forceinline__ void one_env(const EngineP<T>& p, int e, const T* act
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BLOCK, DR ? STEP_MIN_BLOCKS_DR : STEP_MIN_BLOCKS)
-k_step(const __grid_constant__ EngineP<T> p, const T* __restrict__ act, T* __restrict__ obs,
-       T* __restrict__ rew, uint8_t* __restrict__ done, int8_t* __restrict__ reason) {
+k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
+       void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
+       int8_t* __restrict__ reason) {
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     StatAcc st;
     if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason, st);
@@ -325,8 +393,8 @@ k_step(const __grid_constant__ EngineP<T> p, const T* __restrict__ act, T* __res
 // steps envs t and t+BLOCK of that span (both loads stay coalesced).
 template <bool TRACK, bool MIX>
 __global__ void __launch_bounds__(BLOCK, PAIR_MIN_BLOCKS)
-k_step_pair(const __grid_constant__ EngineP<float> p, const float* __restrict__ act,
-            float* __restrict__ obs, float* __restrict__ rew, uint8_t* __restrict__ done,
+k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ act,
+            void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
             int8_t* __restrict__ reason) {
     const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
     StatAcc st;
@@ -456,8 +524,8 @@ __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restri
 // ------------------------------------------------------------------ launchers
 template <class T>
 cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
-                            const T* act, T* obs, T* rew, uint8_t* done, int8_t* reason,
-                            cudaStream_t st) {
+                            const void* act, void* obs, void* rew, uint8_t* done,
+                            int8_t* reason, cudaStream_t st) {
     const bool mix = p.n_veh > 1;
     if constexpr (std::is_same<T, float>::value) {
         if (pair && fossen && !dr) {
