@@ -71,7 +71,8 @@ def bytes_per_env_step(kind: str, n_act: int, obs_dim: int, dr: bool) -> int:
     return b
 
 
-def build_config(name: str, rank: int, precision: str, pair: str = "auto"):
+def build_config(name: str, rank: int, precision: str, pair: str = "auto",
+                 stage_obs: str = "auto"):
     import paper_2410_14117_b200 as uuv
     c = CONFIGS[name]
     n = c["num_envs"]
@@ -89,6 +90,7 @@ def build_config(name: str, rank: int, precision: str, pair: str = "auto"):
         cfg = uuv.engine_config_dict(vdocs[0], spec, n, 0, 0, ranges, precision=precision,
                                      device=rank_device(), env_offset=rank * n)
     cfg["device"]["pair"] = pair
+    cfg["device"]["stage_obs"] = stage_obs
     return cfg, [v.n_thrusters() for v in vdocs]
 
 
@@ -253,6 +255,8 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--pair", default="auto", choices=["auto", "on", "off"],
                     help="two envs per thread (default: auto by env count)")
+    ap.add_argument("--stage-obs", default="auto", choices=["auto", "on", "off"],
+                    help="observation rows through shared memory (default: tracking only)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the secondary config sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
@@ -283,7 +287,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    cfg, n_thr = build_config(args.config, rank, args.precision, args.pair)
+    cfg, n_thr = build_config(args.config, rank, args.precision, args.pair, args.stage_obs)
     c = CONFIGS[args.config]
     env = uuv.B200EnvBatch(cfg)
     n = env.num_envs
@@ -404,7 +408,7 @@ def main():
         for name in ("c4", "c3", "c5"):
             if name == args.config:
                 continue
-            cfg2, nt2 = build_config(name, rank, args.precision, args.pair)
+            cfg2, nt2 = build_config(name, rank, args.precision, args.pair, args.stage_obs)
             e2 = uuv.B200EnvBatch(cfg2)
             a2 = e2.bench_actions_tensor()
             e2.capture_graph(a2, n_steps=1)

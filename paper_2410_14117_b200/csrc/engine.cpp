@@ -323,6 +323,13 @@ void Engine::parse(const std::string& text) {
             else if (s == "off") pair_mode_ = 0;
             else throw ConfigError("device.pair must be \"auto\", \"on\" or \"off\"");
         }
+        if (const json* v = opt(*d, "stage_obs")) {
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "auto") stage_mode_ = -1;
+            else if (s == "on") stage_mode_ = 1;
+            else if (s == "off") stage_mode_ = 0;
+            else throw ConfigError("device.stage_obs must be \"auto\", \"on\" or \"off\"");
+        }
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "dense") force_dense_ = true;
@@ -434,6 +441,10 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.stats = stats_part_;
     p.vpack = d_vpack_;
     p.io_f64 = fp64_ ? 1 : 0;   // device face: engine precision; host ABI: set per launch
+    // staged rows pay off for tracking rows (144 B); station rows (48 B) are
+    // already three 128-bit stores per env (measured)
+    const bool stage_ok = obs_dim_ <= MAX_STAGE_DIM;
+    p.stage_obs = stage_ok && (stage_mode_ == 1 || (stage_mode_ < 0 && obs_dim_ > 12)) ? 1 : 0;
 
     // device buffers carved from the arena
     char* a = static_cast<char*>(arena_);
@@ -888,6 +899,7 @@ std::string Engine::info() const {
         {"randomization", ranges_.enabled},
         {"pattern", fossen_ ? "fossen" : "dense"},
         {"envs_per_thread", pair_ ? 2 : 1},
+        {"stage_obs", (fp64_ ? pd_->stage_obs : pf_->stage_obs) != 0},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},

@@ -28,6 +28,10 @@ constexpr int PAIR_MIN_BLOCKS = UUV_PAIR_MIN_BLOCKS;
 #endif
 constexpr long PAIR_AUTO_MIN_ENVS = UUV_PAIR_AUTO_MIN_ENVS;
 
+// observation staging in shared memory: obs_dim <= MAX_STAGE_DIM (lookahead <= 5)
+constexpr int MAX_STAGE_DIM = 36;
+constexpr int MAX_STAGE_BYTES = 2 * BLOCK * MAX_STAGE_DIM * 8;   // paired block, f64 rows
+
 template <class T> struct Launch {
     // one fused step; fossen selects the structure-specialised variant, pair the
     // two-envs-per-thread kernel (fp32, Fossen, no randomisation)

@@ -71,6 +71,19 @@ __host__ __device__ __forceinline__ uint64_t draw_u64(uint64_t seed, uint64_t st
     return mix64(h ^ counter);
 }
 
+// draw_u64 split: the first three SplitMix rounds depend only on (seed, stream,
+// purpose), so a lane's prefix is hashed once and each counted draw costs one
+// round -- identical bits to draw_u64.
+__host__ __device__ __forceinline__ uint64_t lane_prefix(uint64_t seed, uint64_t stream,
+                                                         uint64_t purpose) {
+    uint64_t h = mix64(seed);
+    h = mix64(h ^ (stream + GOLDEN));
+    return mix64(h ^ (purpose + PURPOSE_SALT));
+}
+__host__ __device__ __forceinline__ uint64_t lane_draw(uint64_t prefix, uint64_t counter) {
+    return mix64(prefix ^ counter);
+}
+
 __host__ __device__ __forceinline__ double u01(uint64_t bits) {
     return (double)(bits >> 11) * (1.0 / 9007199254740992.0);
 }
@@ -166,7 +179,7 @@ template <class T> struct EngineP {
     int32_t act_dim;       // row stride of the action matrix
     int32_t stats_on;
     int32_t io_f64;        // actions / obs / reward are f64 (host ABI path), else T
-    int32_t pad_io;
+    int32_t stage_obs;     // observation rows staged in shared memory, stored coalesced
     // device buffers
     V4<T>* s0; V4<T>* s1; V4<T>* s2;
     int32_t* step;

@@ -127,9 +127,12 @@ __device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ ro
     }
 }
 
+// Dynamic shared memory: observation rows of the block's envs (stage_obs).
+extern __shared__ __align__(16) unsigned char uuv_smem[];
+
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
-__device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t g, T s[12],
-                                           const EnvIn<T, TRACK>& in, bool failed,
+__device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, uint64_t g,
+                                           T s[12], const EnvIn<T, TRACK>& in, bool failed,
                                            void* __restrict__ obs, void* __restrict__ rew,
                                            uint8_t* __restrict__ done,
                                            int8_t* __restrict__ reason, StatAcc& st) {
@@ -166,7 +169,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t 
                 uint64_t pc = p.param_ctr[e];
                 V4<T> n0, n1;
                 V2<T> n2;
-                if (dr_draw<T>(V, p.ranges, seed, g, pc, n0, n1, n2)) {
+                if (dr_draw<T, Pat>(V, p.ranges, seed, g, pc, n0, n1, n2)) {
                     p.dr0[e] = n0; p.dr1[e] = n1; p.dr2[e] = n2;
                 } else {
                     st.n_err += 1;
@@ -189,11 +192,16 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, uint64_t 
 
     // observation (post-reset for finished envs, batch.py:106-118)
     const bool pre = rc < 0 && tk.lookahead <= LA_PRE;
+    // staged: the row goes to shared memory and the block stores all rows
+    // contiguously afterwards (flush_obs); else straight to HBM
+    const size_t D = (size_t)tk.obs_dim;
     if (p.io_f64) {
-        write_obs<T, double, TRACK>(tk, (double*)obs + (size_t)e * tk.obs_dim, s, in, nstep, pre);
+        double* row = p.stage_obs ? (double*)uuv_smem + (size_t)li * D : (double*)obs + (size_t)e * D;
+        write_obs<T, double, TRACK>(tk, row, s, in, nstep, pre);
         ((double*)rew)[e] = (double)reward;
     } else {
-        write_obs<T, T, TRACK>(tk, (T*)obs + (size_t)e * tk.obs_dim, s, in, nstep, pre);
+        T* row = p.stage_obs ? (T*)uuv_smem + (size_t)li * D : (T*)obs + (size_t)e * D;
+        write_obs<T, T, TRACK>(tk, row, s, in, nstep, pre);
         ((T*)rew)[e] = reward;
     }
     done[e] = rc >= 0 ? 1 : 0;
@@ -222,7 +230,7 @@ __device__ __forceinline__ void load_state(const EngineP<T>& p, int e, T s[12]) 
 
 // One env per thread (every precision / pattern / randomisation mode).
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
-__device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
+__device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uint64_t g,
                                          const void* __restrict__ act, void* __restrict__ obs,
                                          void* __restrict__ rew, uint8_t* __restrict__ done,
                                          int8_t* __restrict__ reason, StatAcc& st) {
@@ -278,14 +286,15 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, uint64_t g,
             replay_env<DR, Pat>(p, V, E, e, tau, dt, K, fail_at, s);
         }
     }
-    finish_env<T, TRACK, DR, SLOT, Pat>(p, e, g, s, in, failed, obs, rew, done, reason, st);
+    finish_env<T, TRACK, DR, SLOT, Pat>(p, e, li, g, s, in, failed, obs, rew, done, reason, st);
 }
 
 // Two envs per thread sharing the register-resident vehicle constants (fp32,
 // Fossen pattern, no randomisation): two independent dependency chains per
 // thread hide latency at half the registers of two threads.
 template <bool TRACK, int SLOT>
-__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1,
+__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1, int li0,
+                                          int li1,
                                           const void* __restrict__ act, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
                                           int8_t* __restrict__ reason, StatAcc& st) {
@@ -321,9 +330,9 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
     }
     if (f0 >= 0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, f0, s0);
     if (f1 >= 0) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, f1, s1);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, p.env_offset + (uint64_t)e0, s0, in0,
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, li0, p.env_offset + (uint64_t)e0, s0, in0,
                                                f0 >= 0, obs, rew, done, reason, st);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, p.env_offset + (uint64_t)e1, s1, in1,
+    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, li1, p.env_offset + (uint64_t)e1, s1, in1,
                                                f1 >= 0, obs, rew, done, reason, st);
 }
 
@@ -367,15 +376,40 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
 }
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
-__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, const void* act, void* obs,
-                                        void* rew, uint8_t* done, int8_t* reason, StatAcc& st) {
+__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, int li, const void* act,
+                                        void* obs, void* rew, uint8_t* done, int8_t* reason,
+                                        StatAcc& st) {
     const uint64_t g = p.env_offset + (uint64_t)e;
     bool slot1 = false;
     if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
     if (!slot1)
-        step_env<T, TRACK, DR, 0, Pat>(p, e, g, act, obs, rew, done, reason, st);
+        step_env<T, TRACK, DR, 0, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
     else if constexpr (MIX)
-        step_env<T, TRACK, DR, 1, Pat>(p, e, g, act, obs, rew, done, reason, st);
+        step_env<T, TRACK, DR, 1, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+}
+
+// Store the block's staged observation rows (envs [first, first+n)) with
+// contiguous 128-bit stores: full 128-B lines instead of one partial sector
+// per env and store instruction.
+template <class T>
+__device__ __forceinline__ void flush_obs(const EngineP<T>& p, void* __restrict__ obs, int first,
+                                          int n) {
+    __syncthreads();
+    if (n <= 0) return;
+    const size_t D = (size_t)p.task.obs_dim;
+    const size_t nel = (size_t)n * D;
+    const size_t esz = p.io_f64 ? 8 : sizeof(T);
+    const size_t nbytes = nel * esz;
+    unsigned char* dst = (unsigned char*)obs + (size_t)first * D * esz;
+    if (((uintptr_t)dst & 15) == 0 && (nbytes & 15) == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(uuv_smem);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (size_t i = threadIdx.x; i < nbytes / 16; i += blockDim.x) d4[i] = s4[i];
+    } else {
+        const uint32_t* s1 = reinterpret_cast<const uint32_t*>(uuv_smem);
+        uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
+        for (size_t i = threadIdx.x; i < nbytes / 4; i += blockDim.x) d1[i] = s1[i];
+    }
 }
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
@@ -385,7 +419,12 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
        int8_t* __restrict__ reason) {
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     StatAcc st;
-    if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason, st);
+    if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
+                                                     reason, st);
+    if (p.stage_obs) {
+        const int first = blockIdx.x * BLOCK;
+        flush_obs<T>(p, obs, first, min(BLOCK, p.n_env - first));
+    }
     if (p.stats_on) block_stats(p.stats, st);
 }
 
@@ -401,12 +440,17 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     const bool a0 = e0 < p.n_env, a1 = e1 < p.n_env;
     const int sl0 = MIX && (int64_t)(p.env_offset + (uint64_t)e0) >= p.mix_bound0;
     const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
+    const int l0 = threadIdx.x, l1 = threadIdx.x + BLOCK;
     if (a0 && a1 && sl0 == sl1) {
-        if (sl0 == 0) step_pair<TRACK, 0>(p, e0, e1, act, obs, rew, done, reason, st);
-        else if constexpr (MIX) step_pair<TRACK, 1>(p, e0, e1, act, obs, rew, done, reason, st);
+        if (sl0 == 0) step_pair<TRACK, 0>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
+        else if constexpr (MIX) step_pair<TRACK, 1>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
     } else {
-        if (a0) one_env<float, TRACK, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason, st);
-        if (a1) one_env<float, TRACK, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason, st);
+        if (a0) one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st);
+        if (a1) one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st);
+    }
+    if (p.stage_obs) {
+        const int first = blockIdx.x * (2 * BLOCK);
+        flush_obs<float>(p, obs, first, min(2 * BLOCK, p.n_env - first));
     }
     if (p.stats_on) block_stats(p.stats, st);
 }
@@ -480,8 +524,9 @@ __global__ void __launch_bounds__(BLOCK) k_dr_init(const __grid_constant__ Engin
     uint64_t ctr = 0;
     V4<T> d0, d1;
     V2<T> d2;
-    const bool ok = slot1 ? dr_draw<T>(p.veh[1], p.ranges, p.seed, g, ctr, d0, d1, d2)
-                          : dr_draw<T>(p.veh[0], p.ranges, p.seed, g, ctr, d0, d1, d2);
+    // create-time draw: full 6x6 fp64 check (PatDense) for the error report
+    const bool ok = slot1 ? dr_draw<T, PatDense>(p.veh[1], p.ranges, p.seed, g, ctr, d0, d1, d2)
+                          : dr_draw<T, PatDense>(p.veh[0], p.ranges, p.seed, g, ctr, d0, d1, d2);
     p.dr0[e] = d0; p.dr1[e] = d1; p.dr2[e] = d2;
     p.param_ctr[e] = ctr;
     if (!ok) atomicMin(first_bad, e);
@@ -522,15 +567,28 @@ __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restri
 }
 
 // ------------------------------------------------------------------ launchers
+template <class K>
+static void allow_smem(K kernel) {
+    // opt-in above 48 KB once per kernel variant (paired rows in f64: 73.7 KB)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_STAGE_BYTES);
+}
+
 template <class T>
 cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
                             const void* act, void* obs, void* rew, uint8_t* done,
                             int8_t* reason, cudaStream_t st) {
     const bool mix = p.n_veh > 1;
+    const size_t esz = p.io_f64 ? 8 : sizeof(T);
     if constexpr (std::is_same<T, float>::value) {
         if (pair && fossen && !dr) {
             const dim3 grid((p.n_env + 2 * BLOCK - 1) / (2 * BLOCK));
-#define UUV_P(TR, M) k_step_pair<TR, M><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
+            const size_t smem = p.stage_obs ? (size_t)2 * BLOCK * p.task.obs_dim * esz : 0;
+#define UUV_P(TR, M)                                                                   \
+    do {                                                                               \
+        static bool once = (allow_smem(k_step_pair<TR, M>), true);                     \
+        (void)once;                                                                    \
+        k_step_pair<TR, M><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
+    } while (0)
             if (track) { if (mix) UUV_P(true, true); else UUV_P(true, false); }
             else { if (mix) UUV_P(false, true); else UUV_P(false, false); }
 #undef UUV_P
@@ -538,8 +596,13 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
         }
     }
     const dim3 grid((p.n_env + BLOCK - 1) / BLOCK);
-#define UUV_L(TR, D, M, PAT) \
-    k_step<T, TR, D, M, PAT><<<grid, BLOCK, 0, st>>>(p, act, obs, rew, done, reason)
+    const size_t smem = p.stage_obs ? (size_t)BLOCK * p.task.obs_dim * esz : 0;
+#define UUV_L(TR, D, M, PAT)                                                                 \
+    do {                                                                                     \
+        static bool once = (allow_smem(k_step<T, TR, D, M, PAT>), true);                     \
+        (void)once;                                                                          \
+        k_step<T, TR, D, M, PAT><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
+    } while (0)
 #define UUV_LP(TR, D, M) \
     if (fossen) UUV_L(TR, D, M, PatFossen); else UUV_L(TR, D, M, PatDense)
     if (track) {

@@ -9,8 +9,9 @@ from bench import build_config
 from tools.latency_probe import timed
 
 flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 for nsub in (1, 2, 5, 10, 20):
-    cfg, _ = build_config("c2", 0, "fp32")
+    cfg, _ = build_config(name, 0, "fp32")
     cfg["task"]["n_substeps"] = nsub
     cfg["task"]["control_dt"] = 0.005 * nsub
     env = uuv.B200EnvBatch(cfg)
@@ -29,5 +30,5 @@ for nsub in (1, 2, 5, 10, 20):
         env.replay_graph()
     e1.record(st)
     torch.cuda.synchronize()
-    print(f"n_sub={nsub:3d}: warm {w[1]:.2f} us, flushed {f[1]:.2f} us, in-graph {e0.elapsed_time(e1) * 1e3 / 1000:.2f} us/step")
+    print(f"{name} n_sub={nsub:3d}: warm {w[1]:.2f} us, flushed {f[1]:.2f} us, in-graph {e0.elapsed_time(e1) * 1e3 / 1000:.2f} us/step")
     env.close()
