@@ -323,6 +323,10 @@ void Engine::parse(const std::string& text) {
             else if (s == "off") pair_mode_ = 0;
             else throw ConfigError("device.pair must be \"auto\", \"on\" or \"off\"");
         }
+        if (const json* v = opt(*d, "tma")) {
+            if (!v->is_boolean()) throw ConfigError("device.tma must be a bool");
+            tma_mode_ = v->get<bool>() ? 1 : 0;
+        }
         if (const json* v = opt(*d, "stage_obs")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "auto") stage_mode_ = -1;
@@ -445,6 +449,10 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     // already three 128-bit stores per env (measured)
     const bool stage_ok = obs_dim_ <= MAX_STAGE_DIM;
     p.stage_obs = stage_ok && (stage_mode_ == 1 || (stage_mode_ < 0 && obs_dim_ > 12)) ? 1 : 0;
+    // persistent TMA-pipelined paired kernel (station, no DR, device face)
+    p.persist_blocks = ((tma_mode_ == 1 || (tma_mode_ < 0 && UUV_TMA_PAIR)) && pair_ && task_.kind == 0 &&
+                        !ranges_.enabled && !fp64_ && m_ >= 2 * BLOCK)
+                           ? sm_count_ * TMA_MIN_BLOCKS : 0;
 
     // device buffers carved from the arena
     char* a = static_cast<char*>(arena_);
@@ -882,8 +890,9 @@ void Engine::synchronize() {
 std::string Engine::info() const {
     cudaFuncAttributes a{};
     const bool track = task_.kind != 0, dr = ranges_.enabled, mix = veh_.size() > 1;
-    if (fp64_) Launch<double>::step_attrs(&a, track, dr, fossen_, mix, pair_);
-    else Launch<float>::step_attrs(&a, track, dr, fossen_, mix, pair_);
+    const bool tma = !fp64_ && pf_->persist_blocks > 0;
+    if (fp64_) Launch<double>::step_attrs(&a, track, dr, fossen_, mix, pair_, false);
+    else Launch<float>::step_attrs(&a, track, dr, fossen_, mix, pair_, tma);
     json j = {
         {"engine", "paper_2410_14117_b200"},
         {"abi_version", 1},
@@ -899,6 +908,7 @@ std::string Engine::info() const {
         {"randomization", ranges_.enabled},
         {"pattern", fossen_ ? "fossen" : "dense"},
         {"envs_per_thread", pair_ ? 2 : 1},
+        {"tma_pipelined", (fp64_ ? 0 : pf_->persist_blocks) > 0},
         {"stage_obs", (fp64_ ? pd_->stage_obs : pf_->stage_obs) != 0},
         {"per_episode", ranges_.per_episode},
         {"device", device_},

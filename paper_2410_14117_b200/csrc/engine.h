@@ -121,6 +121,7 @@ private:
     bool force_dense_ = false;
     int pair_mode_ = -1;      // device.pair: -1 auto, 0 off, 1 on
     int stage_mode_ = -1;     // device.stage_obs: -1 auto, 0 off, 1 on
+    int tma_mode_ = -1;       // device.tma: -1 auto, 0 off, 1 on
     bool pair_ = false;       // two envs per thread (resolved)
     int device_ = 0;
     std::vector<BaseVehicle> veh_;

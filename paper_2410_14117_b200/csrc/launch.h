@@ -28,6 +28,18 @@ constexpr int PAIR_MIN_BLOCKS = UUV_PAIR_MIN_BLOCKS;
 #endif
 constexpr long PAIR_AUTO_MIN_ENVS = UUV_PAIR_AUTO_MIN_ENVS;
 
+#ifndef UUV_TMA_MIN_BLOCKS
+#define UUV_TMA_MIN_BLOCKS 5       // persistent TMA pair kernel: 2 x 20 KB stages per block
+#endif
+#ifndef UUV_TMA_ACT
+#define UUV_TMA_ACT 0              // also stage action rows through the TMA ring
+#endif
+#ifndef UUV_TMA_PAIR
+#define UUV_TMA_PAIR 0             // default off: measured slower than the plain paired kernel
+                                   // (96.7 vs 93.7 us at C5; residency 5 vs 6 blocks/SM)
+#endif
+constexpr int TMA_MIN_BLOCKS = UUV_TMA_MIN_BLOCKS;
+
 // observation staging in shared memory: obs_dim <= MAX_STAGE_DIM (lookahead <= 5)
 constexpr int MAX_STAGE_DIM = 36;
 constexpr int MAX_STAGE_BYTES = 2 * BLOCK * MAX_STAGE_DIM * 8;   // paired block, f64 rows
@@ -46,7 +58,7 @@ template <class T> struct Launch {
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
-                                  bool mix, bool pair);
+                                  bool mix, bool pair, bool tma);
     static cudaError_t to_f64(const T* in, double* out, size_t n, cudaStream_t st);
     static cudaError_t from_f64(const double* in, T* out, size_t n, cudaStream_t st);
 };

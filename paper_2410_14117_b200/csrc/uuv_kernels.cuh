@@ -293,17 +293,15 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
 // Fossen pattern, no randomisation): two independent dependency chains per
 // thread hide latency at half the registers of two threads.
 template <bool TRACK, int SLOT>
-__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1, int li0,
-                                          int li1,
-                                          const void* __restrict__ act, void* __restrict__ obs,
+__device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e1, int li0,
+                                          int li1, EnvIn<float, TRACK>& in0,
+                                          EnvIn<float, TRACK>& in1, const void* act0,
+                                          const void* act1, bool io_f64, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
                                           int8_t* __restrict__ reason, StatAcc& st) {
     using Pat = PatFossen;
     const VehP<float>& V = p.veh[SLOT];
     const TaskP<float>& tk = p.task;
-    EnvIn<float, TRACK> in0, in1;
-    load_env<float, TRACK>(p, e0, in0);
-    load_env<float, TRACK>(p, e1, in1);
     float* s0 = in0.s;
     float* s1 = in1.s;
     prewrap(s0);
@@ -318,8 +316,8 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
         load_regs<Pat>(R, E, dt, K);
     }
     float tau0[6], tau1[6];
-    wrench<float, false, REG>(V, E, act_row(p, act, e0), p.io_f64, tau0);
-    wrench<float, false, REG>(V, E, act_row(p, act, e1), p.io_f64, tau1);
+    wrench<float, false, REG>(V, E, act0, io_f64, tau0);
+    wrench<float, false, REG>(V, E, act1, io_f64, tau1);
     int f0 = -1, f1 = -1;
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
@@ -334,6 +332,19 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
                                                f0 >= 0, obs, rew, done, reason, st);
     finish_env<float, TRACK, false, SLOT, Pat>(p, e1, li1, p.env_offset + (uint64_t)e1, s1, in1,
                                                f1 >= 0, obs, rew, done, reason, st);
+}
+
+template <bool TRACK, int SLOT>
+__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1, int li0,
+                                          int li1,
+                                          const void* __restrict__ act, void* __restrict__ obs,
+                                          void* __restrict__ rew, uint8_t* __restrict__ done,
+                                          int8_t* __restrict__ reason, StatAcc& st) {
+    EnvIn<float, TRACK> in0, in1;
+    load_env<float, TRACK>(p, e0, in0);
+    load_env<float, TRACK>(p, e1, in1);
+    pair_core<TRACK, SLOT>(p, e0, e1, li0, li1, in0, in1, act_row(p, act, e0),
+                           act_row(p, act, e1), p.io_f64, obs, rew, done, reason, st);
 }
 
 // Block-level episode statistics: warp reductions -> shared memory -> one
@@ -566,6 +577,130 @@ __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restri
     r[8] = d2.x; r[9] = d2.y;
 }
 
+// ------------------------------------------------------------------ TMA-pipelined paired step
+// Persistent variant of k_step_pair for station tasks on the device face: one
+// elected thread streams the NEXT tile's state planes and action rows into the
+// other half of a two-stage shared-memory ring with 1D bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx), while the whole block computes the
+// current tile -- the HBM traffic of tile i+1 overlaps the sub-steps of tile i
+// instead of every co-resident block loading / computing / storing in lockstep.
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool MIX>
+__global__ void __launch_bounds__(BLOCK, TMA_MIN_BLOCKS)
+k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict__ act,
+                void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
+                int8_t* __restrict__ reason) {
+    constexpr int TILE = 2 * BLOCK;
+    __shared__ __align__(8) uint64_t mbar[2];
+    const int A = p.act_dim;
+    const uint32_t plane_bytes = TILE * 16;
+    const uint32_t act_bytes = UUV_TMA_ACT ? (uint32_t)(TILE * A * 4) : 0u;
+    const uint32_t stage_bytes = 3 * plane_bytes + act_bytes;   // multiple of 16
+    const int n_full = p.n_env / TILE;
+    const float* actf = (const float*)act;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int tile, int stage) {
+        unsigned char* dst = uuv_smem + (size_t)stage * stage_bytes;
+        const size_t base = (size_t)tile * TILE;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[stage], stage_bytes);
+        bulk_g2s(dst, p.s0 + base, plane_bytes, &mbar[stage]);
+        bulk_g2s(dst + plane_bytes, p.s1 + base, plane_bytes, &mbar[stage]);
+        bulk_g2s(dst + 2 * plane_bytes, p.s2 + base, plane_bytes, &mbar[stage]);
+        if (UUV_TMA_ACT) bulk_g2s(dst + 3 * plane_bytes, actf + base * A, act_bytes, &mbar[stage]);
+    };
+    StatAcc st;
+    int stage = 0;
+    uint32_t parity0 = 0, parity1 = 0;
+    int t = blockIdx.x;
+    if (threadIdx.x == 0 && t < n_full) issue(t, 0);
+    for (; t < n_full; t += gridDim.x) {
+        const int nxt = t + gridDim.x;
+        if (threadIdx.x == 0 && nxt < n_full) issue(nxt, stage ^ 1);   // prefetch
+        const int e0 = t * TILE + threadIdx.x, e1 = e0 + BLOCK;
+        EnvIn<float, false> in0, in1;
+        in0.step = p.step[e0]; in1.step = p.step[e1];
+        in0.ep_ret = p.ep_ret[e0]; in1.ep_ret = p.ep_ret[e1];
+        mbar_wait(&mbar[stage], stage ? parity1 : parity0);
+        if (stage) parity1 ^= 1; else parity0 ^= 1;
+        const unsigned char* src = uuv_smem + (size_t)stage * stage_bytes;
+        const float4* q0 = (const float4*)src;
+        const float4* q1 = (const float4*)(src + plane_bytes);
+        const float4* q2 = (const float4*)(src + 2 * plane_bytes);
+        const float* qa = (const float*)(src + 3 * plane_bytes);
+        auto unpack = [&](int li, EnvIn<float, false>& in) {
+            const float4 a0 = q0[li], a1 = q1[li], a2 = q2[li];
+            in.s[0] = a0.x; in.s[1] = a0.y; in.s[2] = a0.z; in.s[3] = a0.w;
+            in.s[4] = a1.x; in.s[5] = a1.y; in.s[6] = a1.z; in.s[7] = a1.w;
+            in.s[8] = a2.x; in.s[9] = a2.y; in.s[10] = a2.z; in.s[11] = a2.w;
+        };
+        unpack(threadIdx.x, in0);
+        unpack(threadIdx.x + BLOCK, in1);
+        const int sl0 = MIX && (int64_t)(p.env_offset + (uint64_t)e0) >= p.mix_bound0;
+        const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
+        const float* r0 = UUV_TMA_ACT ? qa + (size_t)threadIdx.x * A : actf + (size_t)e0 * A;
+        const float* r1 = UUV_TMA_ACT ? qa + (size_t)(threadIdx.x + BLOCK) * A : actf + (size_t)e1 * A;
+        if (sl0 == sl1) {
+            if (sl0 == 0)
+                pair_core<false, 0>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
+                                    reason, st);
+            else if constexpr (MIX)
+                pair_core<false, 1>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
+                                    reason, st);
+        } else {   // vehicle-slab boundary inside the pair: one env at a time
+            if constexpr (MIX) {
+                one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew, done,
+                                                             reason, st);
+                one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew, done,
+                                                             reason, st);
+            }
+        }
+        __syncthreads();   // this stage is consumed before it is refilled
+        stage ^= 1;
+    }
+    // partial tail tile: the block whose turn it is, with plain loads
+    const int tail0 = n_full * TILE;
+    if (tail0 < p.n_env && blockIdx.x == n_full % gridDim.x) {
+        const int e0 = tail0 + threadIdx.x, e1 = e0 + BLOCK;
+        if (e0 < p.n_env) one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew,
+                                                                         done, reason, st);
+        if (e1 < p.n_env) one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew,
+                                                                         done, reason, st);
+    }
+    if (p.stats_on) block_stats(p.stats, st);
+}
+
 // ------------------------------------------------------------------ launchers
 template <class K>
 static void allow_smem(K kernel) {
@@ -580,6 +715,20 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
     const bool mix = p.n_veh > 1;
     const size_t esz = p.io_f64 ? 8 : sizeof(T);
     if constexpr (std::is_same<T, float>::value) {
+        if (pair && fossen && !dr && !track && !p.io_f64 && !p.stage_obs && p.persist_blocks > 0) {
+            const int n_full = p.n_env / (2 * BLOCK);
+            const dim3 grid(std::max(1, std::min(n_full, p.persist_blocks)));
+            const size_t smem = (size_t)2 * (3 * 2 * BLOCK * 16 + (UUV_TMA_ACT ? 2 * BLOCK * p.act_dim * 4 : 0));
+#define UUV_T(M)                                                                        \
+    do {                                                                                \
+        static bool once = (allow_smem(k_step_pair_tma<M>), true);                      \
+        (void)once;                                                                     \
+        k_step_pair_tma<M><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason);  \
+    } while (0)
+            if (mix) UUV_T(true); else UUV_T(false);
+#undef UUV_T
+            return cudaGetLastError();
+        }
         if (pair && fossen && !dr) {
             const dim3 grid((p.n_env + 2 * BLOCK - 1) / (2 * BLOCK));
             const size_t smem = p.stage_obs ? (size_t)2 * BLOCK * p.task.obs_dim * esz : 0;
@@ -655,8 +804,11 @@ cudaError_t Launch<T>::pack_dr(const EngineP<T>& p, double* out, cudaStream_t st
 
 template <class T>
 cudaError_t Launch<T>::step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
-                                  bool mix, bool pair) {
+                                  bool mix, bool pair, bool tma) {
     if constexpr (std::is_same<T, float>::value) {
+        if (pair && fossen && !dr && !track && tma)
+            return mix ? cudaFuncGetAttributes(a, k_step_pair_tma<true>)
+                       : cudaFuncGetAttributes(a, k_step_pair_tma<false>);
         if (pair && fossen && !dr) {
             if (track) return mix ? cudaFuncGetAttributes(a, k_step_pair<true, true>)
                                   : cudaFuncGetAttributes(a, k_step_pair<true, false>);

@@ -354,3 +354,28 @@ def test_kernel_variants(base):
     a, b = engines["single"].states(), engines["dense"].states()
     calm = np.abs(s0[:, 4]) <= P.PITCH_BAND
     assert P.within_tol(b[calm], a[calm], P.STATE_ANGLES).all()
+
+
+def test_tma_pipelined_kernel_bit_identical():
+    """Persistent TMA-pipelined paired kernel == plain paired kernel, bit for bit,
+    over enough tiles that every block loops (and a partial tail tile)."""
+    n = 2 * 128 * 148 * 5 * 2 + 1234
+    base = dict(mixed=True, episode_len=17, n=n, pair="on")
+    cfg_a = _cfg(**base)
+    cfg_a["device"]["tma"] = True
+    a = uuv.B200EnvBatch(cfg_a)
+    cfg_b = _cfg(**base)
+    cfg_b["device"]["tma"] = False
+    b = uuv.B200EnvBatch(cfg_b)
+    assert a.info["tma_pipelined"] and not b.info["tma_pipelined"]
+    act = a.bench_actions_tensor()
+    for _ in range(25):
+        oa, ra, da, qa = a.step_tensors(act)
+        ob, rb, db, qb = b.step_tensors(act)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ob) and torch.equal(ra, rb) and torch.equal(da, db)
+    assert np.array_equal(a.states(), b.states())
+    assert np.array_equal(a.step_counts(), b.step_counts())
+    sa, sb = a.stats(), b.stats()
+    assert sa["env_steps"] == sb["env_steps"] == 25 * n
+    assert sa["done_truncation"] == sb["done_truncation"] > 0
