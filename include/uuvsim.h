@@ -104,6 +104,8 @@ int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, void* obs, uint64_t obs
                          uint64_t stream);
 int32_t uuvsim_dev_observe(uint64_t handle, void* obs, uint64_t obs_len, uint64_t stream);
 int32_t uuvsim_dev_bench_actions(uint64_t handle, void* actions, uint64_t len, uint64_t stream);
+/* raw states [M][12] into a device buffer (engine precision) */
+int32_t uuvsim_dev_states(uint64_t handle, void* out, uint64_t len, uint64_t stream);
 int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,
                          uint64_t stream);
 /* capture n_steps consecutive device steps on fixed buffers into a CUDA graph */

@@ -255,6 +255,16 @@ class B200EnvBatch:
             self._handle, t["obs"].data_ptr(), t["obs"].numel(), self._stream(stream)))
         return t["obs"]
 
+    def states_tensor(self, out=None, stream=None):
+        """Raw states [M, 12] on the device (engine precision), e.g. for PD control."""
+        import torch
+        if out is None:
+            out = torch.empty((self.num_envs, 12), dtype=self.dtype,
+                              device=torch.device("cuda", self.device_index))
+        _core.check(self._lib, self._lib.uuvsim_dev_states(self._handle, out.data_ptr(),
+                                                           out.numel(), self._stream(stream)))
+        return out
+
     def bench_actions_tensor(self, stream=None):
         """Fixed U[-1,1] bench actions (reference batch.py:168-176) generated on device."""
         import torch

@@ -282,6 +282,15 @@ int32_t uuvsim_dev_bench_actions(uint64_t h, void* act, uint64_t len, uint64_t s
     });
 }
 
+int32_t uuvsim_dev_states(uint64_t h, void* out, uint64_t len, uint64_t stream) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t want = (uint64_t)e.num_envs() * 12;
+        if (!out || len != want) return bad_size("states", want, e.is_fp64() ? "f64" : "f32");
+        e.dev_states(out, as_stream(stream));
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_stats(uint64_t h, double* out, uint64_t len, int32_t clear, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         if (!out || len != (uint64_t)uuv::NSTAT) return bad_size("stats", uuv::NSTAT, "f64");

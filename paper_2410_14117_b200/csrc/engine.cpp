@@ -843,6 +843,11 @@ void Engine::dev_observe(void* obs, cudaStream_t st) {
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
 }
 
+void Engine::dev_states(void* out, cudaStream_t st) {
+    if (fp64_) cuda_check(Launch<double>::pack_states_t(*pd_, (double*)out, st), "dev_states");
+    else cuda_check(Launch<float>::pack_states_t(*pf_, (float*)out, st), "dev_states");
+}
+
 void Engine::dev_bench_actions(void* act, cudaStream_t st) {
     const uint64_t seed = fp64_ ? pd_->seed : pf_->seed;
     cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_,

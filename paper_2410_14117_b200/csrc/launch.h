@@ -55,6 +55,7 @@ template <class T> struct Launch {
     static cudaError_t observe(const EngineP<T>& p, T* obs, cudaStream_t st);
     static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);
     static cudaError_t pack_states(const EngineP<T>& p, double* out, cudaStream_t st);
+    static cudaError_t pack_states_t(const EngineP<T>& p, T* out, cudaStream_t st);
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,

@@ -543,12 +543,12 @@ __global__ void __launch_bounds__(BLOCK) k_dr_init(const __grid_constant__ Engin
     if (!ok) atomicMin(first_bad, e);
 }
 
-template <class T>
-__global__ void k_pack_states(const __grid_constant__ EngineP<T> p, double* __restrict__ out) {
+template <class T, class O = double>
+__global__ void k_pack_states(const __grid_constant__ EngineP<T> p, O* __restrict__ out) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.n_env) return;
     const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
-    double* r = out + (size_t)e * 12;
+    O* r = out + (size_t)e * 12;
     r[0] = a0.x; r[1] = a0.y; r[2] = a0.z; r[3] = a0.w;
     r[4] = a1.x; r[5] = a1.y; r[6] = a1.z; r[7] = a1.w;
     r[8] = a2.x; r[9] = a2.y; r[10] = a2.z; r[11] = a2.w;
@@ -786,7 +786,13 @@ cudaError_t Launch<T>::dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t
 
 template <class T>
 cudaError_t Launch<T>::pack_states(const EngineP<T>& p, double* out, cudaStream_t st) {
-    k_pack_states<T><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, out);
+    k_pack_states<T, double><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, out);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::pack_states_t(const EngineP<T>& p, T* out, cudaStream_t st) {
+    k_pack_states<T, T><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, out);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,232 @@
+"""PD baseline (reference pkg/src/uuvsim/baseline.py:21-102).
+
+CPU: the batched torch PD against a per-env restatement of the reference
+formula, the reference-trajectory table against tasks.py:132-153, and the
+SPEC acceptance (SPEC.md:578 -- station-keeping error at 30 s < 0.3x the reset
+error for 100 seeded episodes) on the C oracle driven by the reference-form PD.
+GPU: the same closed loop on the B200 engine (device PD + fused step, one CUDA
+graph per episode) against the oracle driven by the fp64 reference PD.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2410_14117_b200 as uuv
+from paper_2410_14117_b200 import baseline as B
+from oracle import oracle as orc
+
+
+def _ref_pd_one(s, r, kp, kd, pinv, kmax, quad):
+    """baseline.py:50-75, one env, plain math (the reference's own operation order)."""
+    ew = r[0:3] - s[0:3]
+    cphi, sphi = math.cos(s[3]), math.sin(s[3])
+    cth, sth = math.cos(s[4]), math.sin(s[4])
+    cpsi, spsi = math.cos(s[5]), math.sin(s[5])
+    rot = np.array([
+        [cpsi * cth, -spsi * cphi + cpsi * sth * sphi, spsi * sphi + cpsi * cphi * sth],
+        [spsi * cth, cpsi * cphi + sphi * sth * spsi, -cpsi * sphi + sth * spsi * cphi],
+        [-sth, cth * sphi, cth * cphi]])
+    eb = rot.T @ ew
+    ea = (r[3:6] - s[3:6] + np.pi) % (2.0 * np.pi) - np.pi
+    wrench = np.asarray(kp) * np.concatenate([eb, ea]) - np.asarray(kd) * s[6:12]
+    f = pinv @ wrench
+    out = np.empty_like(f)
+    for i in range(len(f)):
+        out[i] = math.copysign(math.sqrt(abs(f[i]) / kmax[i]), f[i]) if quad[i] else f[i] / kmax[i]
+    return np.clip(out, -1.0, 1.0)
+
+
+def _ref_pd_vec(S, r, kp, kd, pinv, kmax, quad):
+    """Vectorised numpy restatement of _ref_pd_one (checked equal below)."""
+    ph, th, ps = S[:, 3], S[:, 4], S[:, 5]
+    cphi, sphi, cth, sth, cpsi, spsi = (np.cos(ph), np.sin(ph), np.cos(th), np.sin(th),
+                                        np.cos(ps), np.sin(ps))
+    rot = np.stack([
+        np.stack([cpsi * cth, -spsi * cphi + cpsi * sth * sphi, spsi * sphi + cpsi * cphi * sth], -1),
+        np.stack([spsi * cth, cpsi * cphi + sphi * sth * spsi, -cpsi * sphi + sth * spsi * cphi], -1),
+        np.stack([-sth, cth * sphi, cth * cphi], -1)], 1)          # [M, 3, 3]
+    ew = r[0:3] - S[:, 0:3]
+    eb = np.einsum("mji,mj->mi", rot, ew)
+    ea = (r[3:6] - S[:, 3:6] + np.pi) % (2.0 * np.pi) - np.pi
+    wrench = np.asarray(kp) * np.concatenate([eb, ea], 1) - np.asarray(kd) * S[:, 6:12]
+    f = wrench @ pinv.T
+    out = np.where(quad, np.copysign(np.sqrt(np.abs(f) / kmax), f), f / kmax)
+    return np.clip(out, -1.0, 1.0)
+
+
+def _consts(params, gains=B.PDGains()):
+    pinv = np.linalg.pinv(B.allocation_matrix(params))
+    kmax, quad = B.thruster_table(params)
+    return gains.kp, gains.kd, pinv, kmax, quad
+
+
+def _random_states(m, seed):
+    rng = np.random.default_rng(seed)
+    s = np.zeros((m, 12))
+    s[:, 0:3] = rng.uniform(-3, 3, (m, 3))
+    s[:, 3:6] = rng.uniform(-4, 4, (m, 3))          # beyond +-pi: exercises the wrap
+    s[:, 6:12] = rng.normal(0, 0.5, (m, 6))
+    return s
+
+
+def test_gains_validation_and_defaults():
+    g = B.PDGains()
+    assert g.kp == (30.0, 30.0, 30.0, 6.0, 6.0, 6.0) and g.kd == (28.0, 28.0, 28.0, 2.0, 2.0, 2.0)
+    with pytest.raises(ValueError):
+        B.PDGains(kp=(1.0,) * 5)
+    with pytest.raises(ValueError):
+        B.PDGains(kd=(1.0, 1.0, 1.0, 1.0, 1.0, float("nan")))
+
+
+def test_allocation_matrix_columns():
+    p = uuv.default_params()
+    a = B.allocation_matrix(p)
+    th = p.to_dict()["thrusters"]
+    assert a.shape == (6, len(th))
+    for i, t in enumerate(th):
+        d, pos = np.asarray(t["direction"]), np.asarray(t["position"])
+        np.testing.assert_array_equal(a[0:3, i], d)
+        np.testing.assert_allclose(a[3:6, i], np.cross(pos, d), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("vehicle", ["heavy", "bluerov2"])
+def test_pd_batch_matches_reference_formula(vehicle):
+    params = uuv.default_params() if vehicle == "heavy" else uuv.bluerov2_params()
+    c = _consts(params)
+    S = _random_states(257, 3)
+    r = np.array([0.3, -0.2, 2.0, 0.1, -0.05, 2.9])
+    want = np.stack([_ref_pd_one(S[i], r, *c) for i in range(len(S))])
+    np.testing.assert_allclose(_ref_pd_vec(S, r, *c), want, rtol=0, atol=1e-13)
+    got = B.pd_batch(torch.from_numpy(S), torch.from_numpy(r), B.PDGains(), params).numpy()
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-12)
+    one = B.pd_baseline(S[5], r, B.PDGains(), params)
+    np.testing.assert_allclose(one, want[5], rtol=0, atol=1e-12)
+    actor = B.PDActor(uuv.TaskSpec(target=tuple(r)), params)
+    np.testing.assert_allclose(actor(None, S, 0), want, rtol=0, atol=1e-12)
+    assert np.all(np.abs(got) <= 1.0) and np.any(np.abs(got) == 1.0)
+
+
+@pytest.mark.parametrize("kind", ["circle", "helix", "lemniscate", "station_keeping"])
+def test_trajectory_table_matches_reference(kind):
+    spec = uuv.TaskSpec(kind=kind, center=(0.5, -0.25))
+    tab = B.trajectory_table(spec, 700).numpy()
+    cx, cy = spec.center
+    for step in (0, 1, 17, 599, 699):
+        t = step * spec.control_dt                              # baseline.py:90-94
+        if kind == "station_keeping":
+            want = np.asarray(spec.target)
+        else:
+            ang = spec.angular_rate * t                         # tasks.py:132-153
+            ca, sa = math.cos(ang), math.sin(ang)
+            if kind in ("circle", "helix"):
+                x, y = cx + spec.radius * ca, cy + spec.radius * sa
+                z = spec.depth + (spec.climb_rate * t if kind == "helix" else 0.0)
+                psi = math.atan2(ca, -sa)
+            else:
+                x, y, z = cx + spec.scale * ca, cy + spec.scale * (sa * ca), spec.depth
+                psi = math.atan2(ca * ca - sa * sa, -sa)
+            want = np.array([x, y, z, 0.0, 0.0, psi])
+        np.testing.assert_allclose(tab[step], want, rtol=0, atol=1e-12)
+
+
+def _oracle_closed_loop(cfg, steps, seed, pd_consts, ref_tab):
+    ob = orc.OracleBatch(cfg, threads=0)
+    ob.reset_all(seed)
+    s0 = ob.states()
+    errs = np.zeros((steps, ob.num_envs))
+    dones = np.zeros((steps, ob.num_envs), dtype=bool)
+    for t in range(steps):
+        act = _ref_pd_vec(ob.states(), ref_tab[t], *pd_consts)
+        _o, r, d = ob.step(act)
+        errs[t], dones[t] = -r, d
+    final = ob.states()
+    ob.close()
+    return s0, errs, dones, final
+
+
+def test_spec_pd_closed_loop_on_oracle():
+    """SPEC.md:578 on the oracle: 100 seeded episodes, default params."""
+    spec = uuv.TaskSpec()
+    params = uuv.default_params()
+    cfg = uuv.engine_config_dict(params, spec, 100, 7, 0, None)
+    tab = B.trajectory_table(spec, spec.episode_len).numpy()
+    s0, errs, dones, _ = _oracle_closed_loop(cfg, spec.episode_len, 7, _consts(params), tab)
+    err0 = np.linalg.norm(tab[0, 0:3] - s0[:, 0:3], axis=1)
+    assert not dones[:-1].any()                       # no termination inside the episode
+    assert dones[-1].all()                            # truncation at step 600
+    assert np.all(errs[-1] < 0.3 * err0), (errs[-1] / err0).max()
+
+
+# ---------------------------------------------------------------- GPU -------
+
+def _gpu_env(cfg):
+    return uuv.B200EnvBatch(cfg, cfg["seed"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["station_heavy", "circle_bluerov2_drep", "station_heavy_fp64"])
+def test_pd_closed_loop_parity(case):
+    kind, vehicle, dr, prec = {
+        "station_heavy": ("station_keeping", "heavy", None, "fp32"),
+        "circle_bluerov2_drep": ("circle", "bluerov2", "episode", "fp32"),
+        "station_heavy_fp64": ("station_keeping", "heavy", None, "fp64"),
+    }[case]
+    spec = uuv.TaskSpec(kind=kind)
+    params = uuv.default_params() if vehicle == "heavy" else uuv.bluerov2_params()
+    ranges = uuv.default_ranges(per_episode=True) if dr else None
+    n, steps, seed = 2048, 600, 11
+    cfg = uuv.engine_config_dict(params, spec, n, seed, 0, ranges, precision=prec, device=0)
+    tab = B.trajectory_table(spec, steps).numpy()
+    s0, errs, dones, final = _oracle_closed_loop(cfg, steps, seed, _consts(params), tab)
+
+    env = _gpu_env(cfg)
+    out = B.evaluate_pd(env, B.PDActor(spec, params), seed, steps)
+    g_final = env.states()
+    env.close()
+    np.testing.assert_array_equal(out["dones"].astype(bool), dones)
+    np.testing.assert_allclose(out["err0"], np.linalg.norm(tab[0, 0:3] - s0[:, 0:3], axis=1),
+                               rtol=1e-6 if prec == "fp32" else 1e-13)
+    # closed-loop drift, fp32 engine + fp32 PD vs fp64 oracle + fp64 PD.  The PD loop
+    # is contracting, so per-step fp32 differences do not accumulate (measured
+    # <= 5e-7 relative on tracking tasks).  Station keeping converges to 3e-11 m in
+    # fp64 but stalls at ~1.3e-5 m in fp32: once dt_sub * v drops below half an ulp
+    # of z = 2 m (1.2e-7 m) the position update rounds away -- hence the 5e-5 m atol.
+    rtol, atol = (2e-5, 5e-5) if prec == "fp32" else (1e-12, 1e-14)
+    e_gpu = np.asarray(out["per_step_error"])
+    np.testing.assert_allclose(e_gpu, errs.mean(1), rtol=rtol, atol=atol)
+    # states after the final (truncating) step are fresh resets: bit-exact in fp64 mode
+    if prec == "fp64":
+        np.testing.assert_array_equal(g_final, final)
+    else:
+        np.testing.assert_allclose(g_final, final, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_spec_pd_closed_loop_on_gpu():
+    """SPEC.md:578 on the B200 engine, device PD, the episode as one CUDA graph."""
+    spec = uuv.TaskSpec()
+    params = uuv.default_params()
+    env = uuv.batch_create(spec, params, None, 100, 7, device=0)
+    out = B.evaluate_pd(env, B.PDActor(spec, params), 7)
+    env.close()
+    assert not out["dones"][:-1].any() and out["dones"][-1].all()
+    assert np.all(out["final_error"] < 0.3 * out["err0"])
+
+
+@pytest.mark.gpu
+def test_pd_graph_equals_eager():
+    spec = uuv.TaskSpec(kind="lemniscate")
+    params = uuv.bluerov2_params()
+    res = []
+    for g in (True, False):
+        env = uuv.batch_create(spec, params, uuv.default_ranges(per_episode=True), 1024, 5,
+                               device=0)
+        res.append(B.evaluate_pd(env, B.PDActor(spec, params), 5, 120, use_graph=g))
+        env.close()
+    np.testing.assert_array_equal(res[0]["per_step_error"], res[1]["per_step_error"])
+    np.testing.assert_array_equal(res[0]["dones"], res[1]["dones"])
