@@ -104,6 +104,11 @@ int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, void* obs, uint64_t obs
                          uint64_t stream);
 int32_t uuvsim_dev_observe(uint64_t handle, void* obs, uint64_t obs_len, uint64_t stream);
 int32_t uuvsim_dev_bench_actions(uint64_t handle, void* actions, uint64_t len, uint64_t stream);
+/* register (buf != NULL) or clear (NULL) a caller-owned device buffer
+ * [M][obs_dim] (engine precision): later device-face steps write each finished
+ * env's TERMINAL observation (pre-reset state, terminating step) into its row;
+ * other rows are left untouched.  Not used by the host-buffer uuvsim_step. */
+int32_t uuvsim_dev_set_final_obs(uint64_t handle, void* buf, uint64_t len);
 /* raw states [M][12] into a device buffer (engine precision) */
 int32_t uuvsim_dev_states(uint64_t handle, void* out, uint64_t len, uint64_t stream);
 int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,

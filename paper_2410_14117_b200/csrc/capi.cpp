@@ -291,6 +291,15 @@ int32_t uuvsim_dev_states(uint64_t h, void* out, uint64_t len, uint64_t stream) 
     });
 }
 
+int32_t uuvsim_dev_set_final_obs(uint64_t h, void* buf, uint64_t len) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
+        if (buf && len != want) return bad_size("final_obs", want, e.is_fp64() ? "f64" : "f32");
+        e.dev_set_final_obs(buf);
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_stats(uint64_t h, double* out, uint64_t len, int32_t clear, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         if (!out || len != (uint64_t)uuv::NSTAT) return bad_size("stats", uuv::NSTAT, "f64");

@@ -444,6 +444,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.stats_on = stats_on_ ? 1 : 0;
     p.stats = stats_part_;
     p.vpack = d_vpack_;
+    p.final_obs = nullptr;
     p.io_f64 = fp64_ ? 1 : 0;   // device face: engine precision; host ABI: set per launch
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are
     // already three 128-bit stores per env (measured)
@@ -678,10 +679,13 @@ void Engine::enqueue_step_host(const double* act, double* obs, double* rew, uint
                "step H2D");
     EngineP<T>& p = P<T>();
     p.io_f64 = 1;
+    void* const fo = p.final_obs;   // terminal obs: device face only
+    p.final_obs = nullptr;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           d_act64_, d_obs64_, d_rew64_, d_done_, d_reason_,
                                           stream_);
     p.io_f64 = fp64_ ? 1 : 0;
+    p.final_obs = fo;
     cuda_check(e, "step");
     cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
     cuda_check(cudaMemcpyAsync(rew, d_rew64_, N * 8, cudaMemcpyDeviceToHost, stream_), "rew D2H");
@@ -841,6 +845,11 @@ void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
 void Engine::dev_observe(void* obs, cudaStream_t st) {
     if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
+}
+
+void Engine::dev_set_final_obs(void* buf) {
+    if (fp64_) pd_->final_obs = buf;
+    else pf_->final_obs = buf;
 }
 
 void Engine::dev_states(void* out, cudaStream_t st) {

@@ -193,6 +193,9 @@ template <class T> struct EngineP {
     // fp32 register pack per vehicle (PACK_F4 float4 each, see uuv_model.cuh
     // load_regs): read once per step with LDG so ptxas keeps it in registers
     const float4* vpack;
+    // optional [n_env][obs_dim] T buffer (device face): finished envs write their
+    // TERMINAL observation (pre-reset state at the terminating step) here
+    void* final_obs;
 };
 
 constexpr int PACK_F4 = 10;   // 40 floats: Fossen pattern + restoring + trig constants

@@ -163,6 +163,10 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
         st.epret += er;
         st.eplen += ns;
         er = 0.0f;
+        if (p.final_obs) {   // terminal observation before the auto-reset (TorchRL / gym)
+            T* row = (T*)p.final_obs + (size_t)e * tk.obs_dim;
+            write_obs<T, T, TRACK>(tk, row, s, in, ns, false);
+        }
         const uint64_t seed = *p.seed_dev;
         if constexpr (DR) {
             if (p.ranges.per_episode) {   // engine.rs:553-558, batch.py:107-110
