@@ -91,6 +91,21 @@ class B200EnvBatch:
         if act.shape != (self.num_envs, self.action_dim):
             raise ValueError(f"actions must have shape {(self.num_envs, self.action_dim)}, "
                              f"got {act.shape}")
+        if getattr(self, "_pool", None) is not None:
+            # fresh page-locked block per step: the engine writes the outputs
+            # straight into it and the returned arrays ARE that block (no host
+            # copy); torch's caching host allocator recycles it once dropped
+            n, d = self.num_envs, self.obs_dim
+            o_rew, o_done, o_rsn, nbytes = self._pool
+            blk = self._torch.empty(nbytes, dtype=self._torch.uint8, pin_memory=True).numpy()
+            base = blk.ctypes.data
+            _core.check(self._lib, self._lib.uuvsim_step_ex(
+                self._handle, act.ctypes.data, act.size, base, n * d, base + o_rew, n,
+                base + o_done, n, base + o_rsn, n))
+            return (blk[:o_rew].view(np.float64).reshape(n, d),
+                    blk[o_rew:o_done].view(np.float64),
+                    blk[o_done:o_done + n].view(np.bool_),
+                    blk[o_rsn:o_rsn + n].view(np.int8))
         if getattr(self, "_bufptrs", None) is None:   # fixed output buffers: marshal once
             self._bufptrs = (self._obs.ctypes.data, self._obs.size, self._rew.ctypes.data,
                              self._rew.size, self._done.ctypes.data, self._done.size,
@@ -148,6 +163,12 @@ class B200EnvBatch:
                         torch.empty(n, dtype=torch.int8, pin_memory=True)]
         self._obs, self._rew, self._done, self._reason = (t.numpy() for t in self._pinned)
         self._bufptrs = None
+        # step outputs: one pinned block per step, [obs f64 | rew f64 | done u8 | reason i8]
+        o_rew = n * self.obs_dim * 8
+        o_done = o_rew + n * 8
+        o_rsn = o_done + n
+        self._pool = (o_rew, o_done, o_rsn, o_rsn + n)
+        self._torch = torch
 
     # -------------------------------------------------------------- inspection / resume
     def set_states(self, states) -> None:

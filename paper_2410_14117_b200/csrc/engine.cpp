@@ -334,6 +334,13 @@ void Engine::parse(const std::string& text) {
             else if (s == "off") stage_mode_ = 0;
             else throw ConfigError("device.stage_obs must be \"auto\", \"on\" or \"off\"");
         }
+        if (const json* v = opt(*d, "host_io")) {
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "auto") host_io_ = -1;
+            else if (s == "copy") host_io_ = 0;
+            else if (s == "mapped") host_io_ = 1;
+            else throw ConfigError("device.host_io must be \"auto\", \"copy\" or \"mapped\"");
+        }
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "dense") force_dense_ = true;
@@ -612,8 +619,10 @@ Engine::~Engine() { release(); }
 void Engine::release() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     graph_exec_ = nullptr;
-    if (abi_graph_.exec) cudaGraphExecDestroy(abi_graph_.exec);
-    abi_graph_ = AbiGraph{};
+    for (AbiGraph& g : abi_graphs_) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = AbiGraph{};
+    }
     if (!fp64_) {
         void* t[] = {d_actT_, d_obsT_, d_rewT_};
         for (void* b : t)
@@ -695,49 +704,130 @@ void Engine::enqueue_step_host(const double* act, double* obs, double* rew, uint
 }
 
 namespace {
-bool page_locked(const void* ptr) {
-    if (!ptr) return true;
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
+// driver query of a host pointer: page-locked?  device alias?  allocation id?
+// (cuPointerGetAttributes through the runtime's entry-point table, so the
+// library has no link-time dependency on libcuda)
+struct HostBuf {
+    bool locked = false;
+    void* dev = nullptr;
+    unsigned long long id = 0;
+};
+using PtrAttrsFn = CUresult (*)(unsigned, CUpointer_attribute*, void**, CUdeviceptr);
+
+PtrAttrsFn ptr_attrs_fn() {
+    static PtrAttrsFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuPointerGetAttributes", &f, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return reinterpret_cast<PtrAttrsFn>(f);
+    }();
+    return fn;
+}
+
+HostBuf host_buf(const void* ptr) {
+    HostBuf b;
+    if (!ptr) {
+        b.locked = true;
+        return b;
     }
-    return a.type == cudaMemoryTypeHost;
+    PtrAttrsFn fn = ptr_attrs_fn();
+    if (!fn) return b;
+    CUpointer_attribute at[3] = {CU_POINTER_ATTRIBUTE_MEMORY_TYPE,
+                                 CU_POINTER_ATTRIBUTE_DEVICE_POINTER,
+                                 CU_POINTER_ATTRIBUTE_BUFFER_ID};
+    unsigned int mt = 0;
+    CUdeviceptr dp = 0;
+    unsigned long long id = 0;
+    void* data[3] = {&mt, &dp, &id};
+    if (fn(3, at, data, (CUdeviceptr)ptr) != CUDA_SUCCESS) return b;
+    b.locked = mt == CU_MEMORYTYPE_HOST;
+    b.dev = b.locked ? (void*)dp : nullptr;
+    b.id = id;
+    return b;
 }
 }  // namespace
+
+// host_io "mapped": the step kernel reads the f64 actions and writes the f64
+// obs / reward / done / reason straight through the caller's page-locked
+// buffers over the host link (zero-copy): one launch + one sync per step,
+// no DMA engine round trips.  Observation rows are staged in shared memory so
+// each block writes one contiguous span.  The caller checked that every buffer
+// is mapped page-locked memory (dev_io_ holds the device aliases).
+template <class T>
+void Engine::step_mapped() {
+    EngineP<T>& p = P<T>();
+    const int32_t io = p.io_f64, stage = p.stage_obs;
+    void* const fo = p.final_obs;
+    p.io_f64 = 1;
+    p.final_obs = nullptr;
+    p.stage_obs = obs_dim_ <= MAX_STAGE_DIM ? 1 : 0;
+    const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
+                                          dev_io_[0], dev_io_[1], dev_io_[2],
+                                          (uint8_t*)dev_io_[3], (int8_t*)dev_io_[4],
+                                          stream_);
+    p.io_f64 = io;
+    p.stage_obs = stage;
+    p.final_obs = fo;
+    cuda_check(e, "step (mapped)");
+    cuda_check(cudaStreamSynchronize(stream_), "step sync");
+}
 
 template <class T>
 void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* done,
                          int8_t* reason) {
-    AbiGraph& g = abi_graph_;
-    const bool same = g.exec && g.act == act && g.obs == obs && g.rew == rew && g.done == done &&
-                      g.reason == reason;
-    if (!same && page_locked(act) && page_locked(obs) && page_locked(rew) && page_locked(done) &&
-        page_locked(reason)) {
-        // (re)capture the whole host-ABI step for these page-locked buffers
-        if (g.exec) cudaGraphExecDestroy(g.exec);
-        g = AbiGraph{};
-        cuda_check(cudaStreamSynchronize(stream_), "abi capture pre-sync");
-        cudaGraph_t graph = nullptr;
-        cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "abi capture");
-        try {
-            enqueue_step_host<T>(act, obs, rew, done, reason);
-        } catch (...) {
-            cudaStreamEndCapture(stream_, &graph);
-            if (graph) cudaGraphDestroy(graph);
-            throw;
-        }
-        cuda_check(cudaStreamEndCapture(stream_, &graph), "abi capture end");
-        const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
-        cudaGraphDestroy(graph);
-        cuda_check(e, "abi graph instantiate");
-        g.act = act; g.obs = obs; g.rew = rew; g.done = done; g.reason = reason;
+    // validated on every call: a cached answer could outlive the caller's buffer
+    const void* ptr[5] = {act, obs, rew, done, reason};
+    HostBuf hb[5];
+    bool locked = true, mapped = true;
+    for (int i = 0; i < 5; ++i) {
+        hb[i] = host_buf(ptr[i]);
+        locked = locked && hb[i].locked;
+        mapped = mapped && (!ptr[i] || hb[i].dev);
+        dev_io_[i] = hb[i].dev;
     }
-    if (g.exec && g.act == act && g.obs == obs && g.rew == rew && g.done == done &&
-        g.reason == reason)
-        cuda_check(cudaGraphLaunch(g.exec, stream_), "abi graph launch");
-    else
-        enqueue_step_host<T>(act, obs, rew, done, reason);   // pageable buffers
+    if (locked && mapped && use_mapped()) {
+        step_mapped<T>();
+        return;
+    }
+    AbiGraph* g = nullptr;
+    if (locked) {
+        for (AbiGraph& c : abi_graphs_) {
+            bool hit = c.exec != nullptr;
+            for (int i = 0; i < 5 && hit; ++i) hit = c.ptr[i] == ptr[i] && c.id[i] == hb[i].id;
+            if (hit) { g = &c; break; }
+        }
+        if (!g) {   // capture the whole host-ABI step for these page-locked buffers
+            g = &abi_graphs_[abi_next_];
+            abi_next_ = (abi_next_ + 1) % kAbiGraphs;
+            if (g->exec) cudaGraphExecDestroy(g->exec);
+            *g = AbiGraph{};
+            cuda_check(cudaStreamSynchronize(stream_), "abi capture pre-sync");
+            cudaGraph_t graph = nullptr;
+            cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal),
+                       "abi capture");
+            try {
+                enqueue_step_host<T>(act, obs, rew, done, reason);
+            } catch (...) {
+                cudaStreamEndCapture(stream_, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            cuda_check(cudaStreamEndCapture(stream_, &graph), "abi capture end");
+            const cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            cuda_check(e, "abi graph instantiate");
+            for (int i = 0; i < 5; ++i) {
+                g->ptr[i] = ptr[i];
+                g->id[i] = hb[i].id;
+            }
+        }
+    }
+    if (g) cuda_check(cudaGraphLaunch(g->exec, stream_), "abi graph launch");
+    else enqueue_step_host<T>(act, obs, rew, done, reason);   // pageable buffers
     cuda_check(cudaStreamSynchronize(stream_), "step sync");
 }
 
@@ -924,6 +1014,7 @@ std::string Engine::info() const {
         {"envs_per_thread", pair_ ? 2 : 1},
         {"tma_pipelined", (fp64_ ? 0 : pf_->persist_blocks) > 0},
         {"stage_obs", (fp64_ ? pd_->stage_obs : pf_->stage_obs) != 0},
+        {"host_io", host_io_ == 0 ? "copy" : host_io_ == 1 ? "mapped" : "auto"},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},

@@ -8,6 +8,7 @@
 // are only touched by the C-ABI copy path.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <array>
@@ -158,14 +159,28 @@ private:
     cudaGraphExec_t graph_exec_ = nullptr;
     // host-ABI step replayed as one CUDA graph (H2D -> step -> D2H) while the
     // caller keeps passing the same page-locked buffers
+    // host_io "mapped": device aliases of the caller's page-locked ABI buffers
+    void* dev_io_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int host_io_ = -1;        // device.host_io: -1 auto, 0 copy, 1 mapped
+    // auto: zero-copy while the per-step host traffic is small enough that
+    // launch + DMA latency dominates (measured crossover)
+    static constexpr size_t kMappedAutoBytes = size_t(8) << 20;
+    bool use_mapped() const {
+        return host_io_ == 1 ||
+               (host_io_ < 0 && (size_t)m_ * (size_t)(obs_dim_ + n_act_ + 2) * 8 <= kMappedAutoBytes);
+    }
+    template <class T> void step_mapped();
+    // whole host-ABI step (H2D, kernel, D2Hs) captured per set of page-locked
+    // buffers; keyed by pointer AND allocation id so a freed-and-reused address
+    // never replays a stale graph.  A few entries: callers alternate buffers.
     struct AbiGraph {
-        const void* act = nullptr;
-        void* obs = nullptr;
-        void* rew = nullptr;
-        void* done = nullptr;
-        void* reason = nullptr;
+        const void* ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        unsigned long long id[5] = {0, 0, 0, 0, 0};
         cudaGraphExec_t exec = nullptr;
-    } abi_graph_;
+    };
+    static constexpr int kAbiGraphs = 4;
+    std::array<AbiGraph, kAbiGraphs> abi_graphs_{};
+    int abi_next_ = 0;
     template <class T> void enqueue_step_host(const double* act, double* obs, double* rew,
                                               uint8_t* done, int8_t* reason);
     std::string device_name_;

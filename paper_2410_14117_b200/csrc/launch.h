@@ -8,7 +8,10 @@
 
 namespace uuv {
 
-constexpr int BLOCK = 128;   // threads per block of the env kernels (one env per thread)
+#ifndef UUV_BLOCK
+#define UUV_BLOCK 128
+#endif
+constexpr int BLOCK = UUV_BLOCK;   // threads per block of the env kernels (one env per thread)
 // register budgets (65536 / (128 * blocks)): measured on B200, see DESIGN.md
 #ifndef UUV_STEP_MIN_BLOCKS
 #define UUV_STEP_MIN_BLOCKS 8      // one env per thread: 64 registers

@@ -113,6 +113,7 @@ BASE = uuv.engine_config_dict(uuv.default_params(), uuv.TaskSpec(), 16, 0)
                                          for i in range(6)]),
      "M_RB + M_A is not positive definite"),
     (lambda c: c["device"].__setitem__("precision", "fp16"), "device.precision"),
+    (lambda c: c["device"].__setitem__("host_io", "dma"), "device.host_io"),
     (lambda c: c.update(vehicles=[c["vehicle"], c["vehicle"]]), "vehicle_mix"),
 ])
 def test_config_errors_are_code_1(lib, mutate, needle):

@@ -1,0 +1,99 @@
+"""Host-ABI step transports (``device.host_io``): DMA copies through a captured
+graph vs zero-copy mapped page-locked buffers.  Both must give bit-identical
+results, with pageable or page-locked caller buffers, and the Python API must
+hand back fresh arrays every step (reference _native.py:159-172 returns copies).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2410_14117_b200 as uuv
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+CASES = {
+    "station_heavy": dict(kind="station_keeping", dr=False, n=4096, L=37),
+    "lemniscate_dr": dict(kind="lemniscate", dr=True, n=3000, L=29),
+    "circle_big": dict(kind="circle", dr=False, n=140000, L=23),   # pair kernel, staged rows
+}
+
+
+def _cfg(case, host_io):
+    c = CASES[case]
+    spec = uuv.TaskSpec(kind=c["kind"], episode_len=c["L"])
+    ranges = uuv.default_ranges(per_episode=True) if c["dr"] else None
+    cfg = uuv.engine_config_dict(uuv.default_params(), spec, c["n"], 5, 0, ranges, device=0)
+    cfg["device"]["host_io"] = host_io
+    return cfg
+
+
+def _run(cfg, steps, pinned):
+    env = uuv.B200EnvBatch(cfg, 5, pinned=pinned)
+    act = uuv.bench_actions(env)
+    if pinned:
+        t = torch.empty(act.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = act
+        act = t.numpy()
+    out = []
+    for _ in range(steps):
+        o, r, d, rs = env.step_ex(act)
+        out.append((o.copy(), r.copy(), d.copy(), rs.copy()))
+    st = env.states()
+    env.close()
+    return out, st
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_copy_and_mapped_are_bit_identical(case):
+    steps = 2 * CASES[case]["L"] + 3          # crosses two episode boundaries
+    ref, st_ref = _run(_cfg(case, "copy"), steps, pinned=False)
+    for mode, pinned in (("copy", True), ("mapped", True), ("auto", True), ("mapped", False)):
+        got, st = _run(_cfg(case, mode), steps, pinned)
+        for a, b in zip(ref, got):
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y), (mode, pinned)
+        assert np.array_equal(st_ref, st)
+
+
+def test_api_returns_fresh_arrays():
+    env = uuv.B200EnvBatch(_cfg("station_heavy", "auto"), 5)
+    act = uuv.bench_actions(env)
+    o1, r1, d1 = env.step(act)
+    keep = (o1.copy(), r1.copy(), d1.copy())
+    o2, r2, d2 = env.step(act)
+    assert not np.shares_memory(o1, o2) and not np.shares_memory(r1, r2)
+    for x, y in zip(keep, (o1, r1, d1)):
+        assert np.array_equal(x, y)            # the first step's arrays were not overwritten
+    assert d2.dtype == np.bool_ and o2.dtype == np.float64 and o2.shape == (4096, 12)
+    env.close()
+
+
+def test_raw_abi_with_alternating_pinned_buffers():
+    """The captured-graph cache is keyed by pointer + allocation id."""
+    cfg = _cfg("station_heavy", "copy")
+    env = uuv.B200EnvBatch(cfg, 5)
+    ref = uuv.B200EnvBatch(cfg, 5, pinned=False)
+    act = uuv.bench_actions(env)
+    lib, h = env._lib, env._handle
+    n, d = env.num_envs, env.obs_dim
+    for i in range(12):
+        bufs = [torch.empty((n, d), dtype=torch.float64, pin_memory=True),
+                torch.empty(n, dtype=torch.float64, pin_memory=True),
+                torch.empty(n, dtype=torch.uint8, pin_memory=True)]
+        if i % 3 == 2:
+            bufs = [b.numpy().copy() for b in bufs]     # pageable every third step
+        arrs = [b if isinstance(b, np.ndarray) else b.numpy() for b in bufs]
+        P = [a.ctypes.data_as(ctypes.c_void_p) for a in arrs]
+        assert lib.uuvsim_step(h, act.ctypes.data_as(ctypes.c_void_p), act.size, P[0], n * d,
+                               P[1], n, P[2], n) == 0
+        o, r, dn = ref.step(act)
+        assert np.array_equal(arrs[0], o) and np.array_equal(arrs[1], r)
+        assert np.array_equal(arrs[2].astype(bool), dn)
+        del bufs, arrs
+    env.close()
+    ref.close()
