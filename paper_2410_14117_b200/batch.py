@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import sys
 import os
 import time
 
@@ -92,20 +93,15 @@ class B200EnvBatch:
             raise ValueError(f"actions must have shape {(self.num_envs, self.action_dim)}, "
                              f"got {act.shape}")
         if getattr(self, "_pool", None) is not None:
-            # fresh page-locked block per step: the engine writes the outputs
-            # straight into it and the returned arrays ARE that block (no host
-            # copy); torch's caching host allocator recycles it once dropped
-            n, d = self.num_envs, self.obs_dim
-            o_rew, o_done, o_rsn, nbytes = self._pool
-            blk = self._torch.empty(nbytes, dtype=self._torch.uint8, pin_memory=True).numpy()
-            base = blk.ctypes.data
+            # outputs land in a page-locked block the engine writes directly
+            # (zero-copy or one DMA); the returned arrays ARE that block, so no
+            # host copy.  A block is reused only once the caller holds none of
+            # its arrays (reference semantics: every step returns fresh arrays)
+            arrs, ptrs = self._free_block()
             _core.check(self._lib, self._lib.uuvsim_step_ex(
-                self._handle, act.ctypes.data, act.size, base, n * d, base + o_rew, n,
-                base + o_done, n, base + o_rsn, n))
-            return (blk[:o_rew].view(np.float64).reshape(n, d),
-                    blk[o_rew:o_done].view(np.float64),
-                    blk[o_done:o_done + n].view(np.bool_),
-                    blk[o_rsn:o_rsn + n].view(np.int8))
+                self._handle, act.ctypes.data, act.size, *ptrs))
+            # a fresh tuple: holding it must count as holding the arrays
+            return arrs[0], arrs[1], arrs[2], arrs[3]
         if getattr(self, "_bufptrs", None) is None:   # fixed output buffers: marshal once
             self._bufptrs = (self._obs.ctypes.data, self._obs.size, self._rew.ctypes.data,
                              self._rew.size, self._done.ctypes.data, self._done.size,
@@ -163,12 +159,35 @@ class B200EnvBatch:
                         torch.empty(n, dtype=torch.int8, pin_memory=True)]
         self._obs, self._rew, self._done, self._reason = (t.numpy() for t in self._pinned)
         self._bufptrs = None
-        # step outputs: one pinned block per step, [obs f64 | rew f64 | done u8 | reason i8]
-        o_rew = n * self.obs_dim * 8
+        # step outputs: pool of pinned blocks [obs f64 | rew f64 | done u8 | reason i8]
+        self._pool = []
+        self._torch = torch
+
+    def _new_block(self):
+        n, d = self.num_envs, self.obs_dim
+        o_rew = n * d * 8
         o_done = o_rew + n * 8
         o_rsn = o_done + n
-        self._pool = (o_rew, o_done, o_rsn, o_rsn + n)
-        self._torch = torch
+        t = self._torch.empty(o_rsn + n, dtype=self._torch.uint8, pin_memory=True)
+        blk = t.numpy()
+        base = blk.ctypes.data
+        arrs = (blk[:o_rew].view(np.float64).reshape(n, d), blk[o_rew:o_done].view(np.float64),
+                blk[o_done:o_rsn].view(np.bool_), blk[o_rsn:o_rsn + n].view(np.int8))
+        ptrs = (base, n * d, base + o_rew, n, base + o_done, n, base + o_rsn, n)
+        return [t, blk, (arrs, ptrs), None]
+
+    _POOL_MAX = 8
+
+    def _free_block(self):
+        """A pool block the caller holds no array (or sub-view) of."""
+        for entry in self._pool:
+            if _pool_refs(entry) == entry[3]:
+                return entry[2]
+        entry = self._new_block()
+        entry[3] = _pool_refs(entry)     # reference counts while only the pool holds it
+        if len(self._pool) < self._POOL_MAX:
+            self._pool.append(entry)
+        return entry[2]
 
     # -------------------------------------------------------------- inspection / resume
     def set_states(self, states) -> None:
@@ -328,6 +347,15 @@ def resolve_backend(backend: str | None = None) -> str:
         raise RuntimeError("this package is the B200 engine; the pure-Python backend lives in "
                            "the reference package (there is no CPU fallback here)")
     raise ValueError(f"unknown backend {choice!r}")
+
+
+def _pool_refs(entry):
+    """Reference counts of a pool block and of each array handed out from it:
+    a returned array the caller keeps raises its own count, any slice / view of
+    it raises the block's (numpy collapses view bases onto the block)."""
+    arrs = entry[2][0]
+    return (sys.getrefcount(entry[1]), sys.getrefcount(arrs[0]), sys.getrefcount(arrs[1]),
+            sys.getrefcount(arrs[2]), sys.getrefcount(arrs[3]))
 
 
 def batch_create(spec: TaskSpec, base, ranges: RandomizationRanges | None, num_envs: int,

@@ -169,7 +169,7 @@ private:
         return host_io_ == 1 ||
                (host_io_ < 0 && (size_t)m_ * (size_t)(obs_dim_ + n_act_ + 2) * 8 <= kMappedAutoBytes);
     }
-    template <class T> void step_mapped();
+    template <class T> void enqueue_step_mapped();
     // whole host-ABI step (H2D, kernel, D2Hs) captured per set of page-locked
     // buffers; keyed by pointer AND allocation id so a freed-and-reused address
     // never replays a stale graph.  A few entries: callers alternate buffers.

@@ -73,6 +73,31 @@ def test_api_returns_fresh_arrays():
     env.close()
 
 
+def test_api_pool_never_overwrites_held_outputs():
+    env = uuv.B200EnvBatch(_cfg("station_heavy", "auto"), 5)
+    ref = uuv.B200EnvBatch(_cfg("station_heavy", "copy"), 5, pinned=False)
+    act = uuv.bench_actions(env)
+    held = []
+    for i in range(12):
+        out = env.step_ex(act)
+        want = ref.step_ex(act)
+        if i % 4 == 0:
+            held.append((out, [w.copy() for w in want]))        # the whole tuple
+        elif i % 4 == 1:
+            held.append((out[0][5:9], want[0][5:9].copy()))     # a sub-view only
+        elif i % 4 == 2:
+            held.append((out[1], want[1].copy()))               # one array
+    for got, want in held:
+        if isinstance(got, tuple):
+            for g, w in zip(got, want):
+                assert np.array_equal(g, w)
+        else:
+            assert np.array_equal(got, want)
+    assert len(env._pool) <= env._POOL_MAX
+    env.close()
+    ref.close()
+
+
 def test_raw_abi_with_alternating_pinned_buffers():
     """The captured-graph cache is keyed by pointer + allocation id."""
     cfg = _cfg("station_heavy", "copy")

@@ -119,13 +119,14 @@ def main():
         obs_dim = 12 if c["kind"] == "station_keeping" else 36
         alg_b = bytes_per_env_step(c["kind"], n_act, obs_dim, bool(c["dr"]))
         fl = flops_per_env_step(c["kind"], n_thr)
-        ex = sum(float(v.get(f"sm__sass_thread_inst_executed_op_{o}_pred_on.sum", 0)) *
-                 (2 if o == "ffma" else 1) for o in ("ffma", "fmul", "fadd"))
+        by = mix(rep)
+        per = n / 32                     # warp-instructions -> thread-instructions per env
+        ex = (2 * by.get("FFMA", 0) + by.get("FMUL", 0) + by.get("FADD", 0)) / per
         out += ["", f"* DRAM traffic per env-step: {(rd + wr) / n:.1f} B (algorithmic minimum "
                 f"{alg_b} B; below it when L2 still holds dirty lines at kernel end)",
                 f"* FP32 work per env-step: algorithmic {fl:.0f} flop (reference dense count),"
-                f" executed {ex / n:.0f} flop (SASS FFMA x2 + FMUL + FADD)", ""]
-        by = mix(rep)
+                f" executed {ex:.0f} flop (SASS FFMA x2 + FMUL + FADD; the structure-"
+                f"specialised kernel skips the reference's exact-zero terms)", ""]
         warps = n / 32 / (2 if "pair" in v.get("Kernel Name", "") else 1)
         tot = sum(by.values())
         out += [f"Executed warp-instructions per env-step: **{tot / (n / 32):.0f}**", "",
