@@ -382,7 +382,8 @@ def main():
                          "note": "back-to-back graph replays, L2 not flushed"},
         "e2e": {"value": e2e_value, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": k_e2e,
-                "path": "uuvsim_step C ABI v1, pinned host f64 buffers"},
+                "path": "B200EnvBatch.step -> uuvsim_step_ex (C ABI v1), page-locked host f64 "
+                        f"buffers, device.host_io={env.info.get('host_io', '?')}"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "traffic": profile_traffic(args.config),
