@@ -137,7 +137,12 @@ def main():
     for lp in a.launches:
         dur = launch_share(lp)
         tot = sum(sum(x) for x in dur.values())
+        harness = sum(sum(x) for k2, x in dur.items() if k2.startswith("at::"))
+        step = sum(sum(x) for k2, x in dur.items() if k2.startswith("uuv::k_step"))
         out += [f"## launch list `{Path(lp).name}` (gpu__time_duration, cold, serialised)", "",
+                "`at::*` kernels are bench.py's 256 MiB L2-flush writes between timed steps"
+                " (harness, not the step); without them the step kernel is "
+                f"{step / max(tot - harness, 1e-9):.1%} of the device time.", "",
                 "| kernel | launches | mean us | share |", "|---|---|---|---|"]
         for k2, xs in sorted(dur.items(), key=lambda kv: -sum(kv[1])):
             out.append(f"| {k2[:60]} | {len(xs)} | {sum(xs) / len(xs) / 1e3:.2f} | "
