@@ -1,0 +1,142 @@
+"""Edge cases of the step the reference defines (tasks.py:201-230,
+dynamics.py:246-306, thrusters.py:97-119): non-finite inputs, out-of-range and
+infinite throttles, integration failure mid-step (last finite state kept,
+reason 2), tiny and ragged batches.  GPU results are compared with the oracle
+(bit-exact for done / reason / counters, tolerance for floats) or, where fp32
+and fp64 fail at different sub-steps, with a self-consistent fp32 construction.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2410_14117_b200 as uuv
+from oracle import oracle as orc
+from tests import parity as P
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _cfg(n=512, kind="station_keeping", precision="fp32", **task):
+    spec = uuv.TaskSpec(kind=kind, **task)
+    return uuv.engine_config_dict(uuv.default_params(), spec, n, 9, 0, None,
+                                  precision=precision, device=0)
+
+
+def _pair(cfg):
+    g = uuv.B200EnvBatch(cfg, cfg["seed"], pinned=False)
+    o = orc.OracleBatch(cfg, threads=0)
+    g.reset_all(cfg["seed"])
+    o.reset_all(cfg["seed"])
+    return g, o
+
+
+def _fp32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_nonfinite_and_out_of_range_actions(precision):
+    cfg = _cfg(precision=precision)
+    g, o = _pair(cfg)
+    n, a = g.num_envs, g.action_dim
+    act = orc.bench_actions(9, n, a)
+    act[::7, 0] = np.nan                    # NaN passes the clamp (ref: t > 1 / t < -1 false)
+    act[1::7, 1] = np.inf                   # clamped to +1
+    act[2::7, 2] = -np.inf                  # clamped to -1
+    act[3::7, :] *= 50.0                    # far outside [-1, 1]
+    act = _fp32(act) if precision == "fp32" else act
+    for _ in range(3):
+        go, gr, gd, grs = g.step_ex(act)
+        oo, orw, od, ors = o.step(act, with_reason=True)
+        assert np.array_equal(gd, od) and np.array_equal(grs, ors)
+        np.testing.assert_allclose(gr, orw, rtol=P.REL_TOL, atol=P.ABS_TOL)
+    # every NaN env failed on its first sub-step (reason 2) and was reset
+    assert np.all(ors[::7] == 2)
+    rc_g, pc_g = g.counters()
+    rc_o, pc_o = o.counters()
+    assert np.array_equal(rc_g, rc_o) and np.array_equal(pc_g, pc_o)
+    sg, so = g.states(), o.states()
+    # failed envs were re-drawn: reset states equal fp32 of the oracle's fp64 draw
+    want = _fp32(so[::7]) if precision == "fp32" else so[::7]
+    assert np.array_equal(sg[::7], want)
+    g.close()
+    o.close()
+
+
+def test_nonfinite_state_fails_and_keeps_last_finite_state():
+    cfg = _cfg(n=300)
+    g, o = _pair(cfg)
+    s = o.states()
+    s[::5, 9] = np.nan                      # NaN roll rate
+    s[1::5, 6] = np.inf                     # infinite surge velocity
+    g.set_states(s)
+    o.set_states(_fp32(s))
+    act = _fp32(orc.bench_actions(9, g.num_envs, g.action_dim))
+    go, gr, gd, grs = g.step_ex(act)
+    oo, orw, od, ors = o.step(act, with_reason=True)
+    assert np.array_equal(grs, ors) and np.all(grs[::5] == 2) and np.all(grs[1::5] == 2)
+    # the reward of a failed env is taken at its last finite (= initial) state
+    np.testing.assert_allclose(gr, orw, rtol=P.REL_TOL, atol=P.ABS_TOL)
+    g.close()
+    o.close()
+
+
+def test_failure_mid_step_keeps_last_finite_substep():
+    """fp32 overflow in sub-step k > 1: the reward and the terminal observation
+    must be those of the state after k-1 sub-steps.  fp64 would overflow at a
+    different sub-step, so the expectation is built from fp32 runs of the same
+    engine with n_substeps = k-1 and k at the same sub_dt."""
+    from paper_2410_14117_b200.torchrl_env import VecEnv
+
+    def run(n_sub, states):
+        cfg = _cfg(n=64, control_dt=0.005 * n_sub, n_substeps=n_sub)
+        vec = VecEnv(uuv.B200EnvBatch(cfg, 9, pinned=False))
+        vec.reset(9)
+        vec.batch.set_states(states)
+        act = torch.zeros((64, vec.action_dim), device=vec.device)
+        out = vec.step(act)
+        res = (out.reward.double().cpu().numpy(), out.reason.cpu().numpy(),
+               out.next_obs.double().cpu().numpy())
+        vec.close()
+        return res
+
+    assert np.float32(0.05 / 10) == np.float32(0.005 * 3 / 3)
+    base = uuv.B200EnvBatch(_cfg(n=64), 9, pinned=False)
+    s = base.states()
+    base.close()
+    s[:, 6] = np.linspace(2e17, 6e18, 64)   # surge: quadratic damping overflows within a few sub-steps
+    r10, why10, obs10 = run(10, s)
+    assert np.all(why10 == 2)
+    first_fail = np.full(64, 99)
+    prefix = {}
+    for k in range(1, 10):
+        rk, whyk, obsk = run(k, s)
+        prefix[k] = (rk, obsk)
+        first_fail[(whyk == 2) & (first_fail == 99)] = k
+    first_fail[first_fail == 99] = 10
+    assert np.any(first_fail > 1)
+    for e in range(64):
+        k = first_fail[e]
+        if k == 1:                          # failed at once: the initial state is kept
+            continue
+        rk, obsk = prefix[k - 1]
+        assert r10[e] == rk[e], (e, k)
+        assert np.array_equal(obs10[e], obsk[e]), (e, k)
+
+
+@pytest.mark.parametrize("n", [1, 31, 129, 257])
+def test_tiny_and_ragged_batches(n):
+    cfg = _cfg(n=n, kind="circle", episode_len=7)
+    g, o = _pair(cfg)
+    act = _fp32(orc.bench_actions(9, n, g.action_dim))
+    for _ in range(15):                     # two truncations
+        _, gr, gd, grs = g.step_ex(act)
+        _, orw, od, ors = o.step(act, with_reason=True)
+        assert np.array_equal(gd, od) and np.array_equal(grs, ors)
+        np.testing.assert_allclose(gr, orw, rtol=1e-4, atol=1e-5)
+    assert np.array_equal(g.step_counts(), o.step_counts())
+    g.close()
+    o.close()
