@@ -387,6 +387,23 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
             V.chol_inv[i] = (T)(1.0 / L[i * 6 + i]);
             V.dquad[i] = (T)v.dquad[i];
         }
+        {   // sub_dt * M_total^-1 on the Fossen pattern (2x2 blocks {0,4}, {1,3}; 2; 5),
+            // in fp64 from the fp64 matrix, then rounded (fp32 product kernel)
+            const double dt = (double)(T)(task_.control_dt / (double)task_.n_substeps);
+            const int blk[2][2] = {{0, 4}, {1, 3}};
+            for (const auto& bk : blk) {
+                const int i = bk[0], j = bk[1];
+                const double a = m_total[i * 6 + i], b = m_total[i * 6 + j];
+                const double c = m_total[j * 6 + i], d = m_total[j * 6 + j];
+                const double id = dt / (a * d - b * c);
+                V.kdt[i * 6 + i] = (T)(d * id);
+                V.kdt[i * 6 + j] = (T)(-b * id);
+                V.kdt[j * 6 + i] = (T)(-c * id);
+                V.kdt[j * 6 + j] = (T)(a * id);
+            }
+            V.kdt[2 * 6 + 2] = (T)(dt / m_total[2 * 6 + 2]);
+            V.kdt[5 * 6 + 5] = (T)(dt / m_total[5 * 6 + 5]);
+        }
         V.weight = (T)v.weight;
         V.buoyancy = (T)v.buoyancy;
         for (int k = 0; k < 3; ++k) {

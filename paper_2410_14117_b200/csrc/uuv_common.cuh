@@ -123,6 +123,7 @@ template <class T> struct VehP {
     T ma[36];        // M_A alone  (scaled by f_added)
     T chol[36];      // lower Cholesky factor of mtot (row-major, lower triangle)
     T chol_inv[6];   // 1 / L_ii
+    T kdt[36];       // sub_dt * M_total^-1 on the Fossen pattern (fp32 product path)
     T dlin[36];
     T dquad[6];
     T weight, buoyancy;

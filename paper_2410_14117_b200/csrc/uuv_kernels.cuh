@@ -33,17 +33,28 @@ __device__ __forceinline__ void prewrap(float s[12]) {
     }
 }
 
+// Rare path: the step ended non-finite.  Re-run it from the step-initial state
+// (still in HBM) with a check after every sub-step and keep the last finite
+// state (the reference stops at the first failing sub-step, model.rs:186-193).
 template <bool DR, class Pat>
 __device__ __forceinline__ void replay_env(const EngineP<float>& p, const VehP<float>& V,
                                         const EnvParams<float, DR || (UUV_PACK_CONSTS && Pat::fossen)>& E, int e,
-                                        const float tau[6], float dt, const TrigK& K, int n,
+                                        const float tau[6], float dt, const TrigK& K, int n_sub,
                                         float s[12]) {
     const V4<float> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
     const float r[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
 #pragma unroll
     for (int i = 0; i < 12; ++i) s[i] = r[i];
     prewrap(s);
-    for (int k = 0; k < n; ++k) substep_fused<DR, Pat>(V, E, s, tau, dt, K);
+#pragma unroll 1
+    for (int k = 0; k < n_sub; ++k) {
+        float t[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) t[i] = s[i];
+        if (!substep_fused<DR, Pat, true>(V, E, t, tau, dt, K)) break;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) s[i] = t[i];
+    }
 }
 
 // Per-thread episode-statistics accumulator (one or two envs per thread).
@@ -259,7 +270,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
     if constexpr (DR) {
         const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
         const V2<T> d2 = p.dr2[e];
-        build_env<T, Pat>(V, d0, d1, d2, E);
+        build_env<T, Pat>(V, d0, d1, d2, (T)tk.sub_dt, E);
     }
     T tau[6];
     wrench<T, DR, REG>(V, E, act_row(p, act, e), p.io_f64, tau);
@@ -279,15 +290,11 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
         // recorded and the env replayed from its initial state (still in HBM)
         // up to the last finite sub-step
         const float dt = dt32;
-        int fail_at = -1;
 #pragma unroll 1
-        for (int k = 0; k < tk.n_substeps; ++k) {
-            const bool ok = substep_fused<DR, Pat>(V, E, s, tau, dt, K);
-            fail_at = (!ok && fail_at < 0) ? k : fail_at;
-        }
-        if (fail_at >= 0) {
+        for (int k = 0; k < tk.n_substeps; ++k) substep_fused<DR, Pat, false>(V, E, s, tau, dt, K);
+        if (!all_finite12(s)) {
             failed = true;
-            replay_env<DR, Pat>(p, V, E, e, tau, dt, K, fail_at, s);
+            replay_env<DR, Pat>(p, V, E, e, tau, dt, K, tk.n_substeps, s);
         }
     }
     finish_env<T, TRACK, DR, SLOT, Pat>(p, e, li, g, s, in, failed, obs, rew, done, reason, st);
@@ -322,20 +329,18 @@ __device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e
     float tau0[6], tau1[6];
     wrench<float, false, REG>(V, E, act0, io_f64, tau0);
     wrench<float, false, REG>(V, E, act1, io_f64, tau1);
-    int f0 = -1, f1 = -1;
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
-        const bool ok0 = substep_fused<false, Pat>(V, E, s0, tau0, dt, K);
-        const bool ok1 = substep_fused<false, Pat>(V, E, s1, tau1, dt, K);
-        f0 = (!ok0 && f0 < 0) ? k : f0;
-        f1 = (!ok1 && f1 < 0) ? k : f1;
+        substep_fused<false, Pat, false>(V, E, s0, tau0, dt, K);
+        substep_fused<false, Pat, false>(V, E, s1, tau1, dt, K);
     }
-    if (f0 >= 0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, f0, s0);
-    if (f1 >= 0) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, f1, s1);
+    const bool f0 = !all_finite12(s0), f1 = !all_finite12(s1);
+    if (f0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, tk.n_substeps, s0);
+    if (f1) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, tk.n_substeps, s1);
     finish_env<float, TRACK, false, SLOT, Pat>(p, e0, li0, p.env_offset + (uint64_t)e0, s0, in0,
-                                               f0 >= 0, obs, rew, done, reason, st);
+                                               f0, obs, rew, done, reason, st);
     finish_env<float, TRACK, false, SLOT, Pat>(p, e1, li1, p.env_offset + (uint64_t)e1, s1, in1,
-                                               f1 >= 0, obs, rew, done, reason, st);
+                                               f1, obs, rew, done, reason, st);
 }
 
 template <bool TRACK, int SLOT>
