@@ -71,15 +71,21 @@ struct StatAcc {
 // the LA_PRE+1 trajectory rows the reward and observation will need).
 constexpr int LA_PRE = 5;
 
-template <class T, bool TRACK> struct EnvIn {
+// RR: the LA_PRE+1 trajectory rows ride in registers across the sub-steps.
+// Where registers are short (randomised or paired kernels) ptxas would park
+// them in local memory -- an STL that waits for the loads before the first
+// sub-step, then LDLs -- so there the prologue only prefetches their cache
+// lines into L1 and finish_env reads the table (L1 hits).
+template <class T, bool TRACK, bool RR = TRACK> struct EnvIn {
+    static constexpr bool kRegRows = TRACK && RR;
     T s[12];
     int32_t step;
     float ep_ret;
-    V4<T> rows[TRACK ? LA_PRE + 1 : 1];   // traj[step+1 .. step+1+LA_PRE]
+    V4<T> rows[kRegRows ? LA_PRE + 1 : 1];   // traj[step+1 .. step+1+LA_PRE]
 };
 
-template <class T, bool TRACK>
-__device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TRACK>& in) {
+template <class T, bool TRACK, bool RR>
+__device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TRACK, RR>& in) {
     const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
     in.s[0] = a0.x; in.s[1] = a0.y; in.s[2] = a0.z; in.s[3] = a0.w;
     in.s[4] = a1.x; in.s[5] = a1.y; in.s[6] = a1.z; in.s[7] = a1.w;
@@ -88,17 +94,24 @@ __device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TR
     in.ep_ret = p.ep_ret[e];
     if constexpr (TRACK) {
         const int tab_last = p.task.episode_len + p.task.lookahead;
+        if constexpr (EnvIn<T, TRACK, RR>::kRegRows) {
 #pragma unroll
-        for (int k = 0; k <= LA_PRE; ++k)
-            in.rows[k] = p.task.traj[min(max(in.step + 1 + k, 0), tab_last)];
+            for (int k = 0; k <= LA_PRE; ++k)
+                in.rows[k] = p.task.traj[min(max(in.step + 1 + k, 0), tab_last)];
+        } else {   // rows step+1 .. step+1+LA_PRE span at most two 128-byte lines
+            const V4<T>* r0 = p.task.traj + min(max(in.step + 1, 0), tab_last);
+            const V4<T>* r1 = p.task.traj + min(max(in.step + 1 + LA_PRE, 0), tab_last);
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r1));
+        }
     }
 }
 
 // observation row of one env (post-reset for finished envs, batch.py:106-118),
 // stored as O = T (device face) or double (host ABI)
-template <class T, class O, bool TRACK>
+template <class T, class O, bool TRACK, class IN>
 __device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ row, const T s[12],
-                                          const EnvIn<T, TRACK>& in, int32_t nstep, bool pre) {
+                                          const IN& in, int32_t nstep, bool pre) {
     if constexpr (!TRACK) {
         V4<O>* o4 = reinterpret_cast<V4<O>*>(row);
         o4[0] = V4<O>{(O)(tk.target[0] - s[0]), (O)(tk.target[1] - s[1]),
@@ -111,15 +124,17 @@ __device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ ro
         V2<O>* o2 = reinterpret_cast<V2<O>*>(row);
         const O ephi = (O)obs_wrap<T>(T(0) - s[3]);
         const O eth = (O)obs_wrap<T>(T(0) - s[4]);
-        if (pre) {   // trajectory rows prefetched by load_env
+        if (IN::kRegRows && pre) {   // trajectory rows prefetched by load_env
+            if constexpr (IN::kRegRows) {
 #pragma unroll
-            for (int k = 1; k <= LA_PRE; ++k) {
-                if (k > tk.lookahead) break;
-                const V4<T> r = in.rows[k];
-                V2<O>* q = o2 + 3 * (k - 1);
-                q[0] = V2<O>{(O)(r.x - s[0]), (O)(r.y - s[1])};
-                q[1] = V2<O>{(O)(r.z - s[2]), ephi};
-                q[2] = V2<O>{eth, (O)obs_wrap<T>(r.w - s[5])};
+                for (int k = 1; k <= LA_PRE; ++k) {
+                    if (k > tk.lookahead) break;
+                    const V4<T> r = in.rows[k];
+                    V2<O>* q = o2 + 3 * (k - 1);
+                    q[0] = V2<O>{(O)(r.x - s[0]), (O)(r.y - s[1])};
+                    q[1] = V2<O>{(O)(r.z - s[2]), ephi};
+                    q[2] = V2<O>{eth, (O)obs_wrap<T>(r.w - s[5])};
+                }
             }
         } else {
 #pragma unroll 1
@@ -141,9 +156,9 @@ __device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ ro
 // Dynamic shared memory: observation rows of the block's envs (stage_obs).
 extern __shared__ __align__(16) unsigned char uuv_smem[];
 
-template <class T, bool TRACK, bool DR, int SLOT, class Pat>
+template <class T, bool TRACK, bool DR, int SLOT, class Pat, class IN>
 __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, uint64_t g,
-                                           T s[12], const EnvIn<T, TRACK>& in, bool failed,
+                                           T s[12], const IN& in, bool failed,
                                            void* __restrict__ obs, void* __restrict__ rew,
                                            uint8_t* __restrict__ done,
                                            int8_t* __restrict__ reason, StatAcc& st) {
@@ -155,7 +170,9 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     const int tab_last = tk.episode_len + tk.lookahead;
     T rx, ry, rz;
     if constexpr (TRACK) {
-        const V4<T> r = in.rows[0];
+        V4<T> r;
+        if constexpr (IN::kRegRows) r = in.rows[0];
+        else r = tk.traj[min(max(ns, 0), tab_last)];
         rx = r.x; ry = r.y; rz = r.z;
     } else {
         rx = tk.target[0]; ry = tk.target[1]; rz = tk.target[2];
@@ -206,7 +223,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
 
     // observation (post-reset for finished envs, batch.py:106-118)
-    const bool pre = rc < 0 && tk.lookahead <= LA_PRE;
+    const bool pre = IN::kRegRows && rc < 0 && tk.lookahead <= LA_PRE;
     // staged: the row goes to shared memory and the block stores all rows
     // contiguously afterwards (flush_obs); else straight to HBM
     const size_t D = (size_t)tk.obs_dim;
@@ -251,7 +268,7 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
                                          int8_t* __restrict__ reason, StatAcc& st) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
-    EnvIn<T, TRACK> in;
+    EnvIn<T, TRACK, !DR> in;
     load_env<T, TRACK>(p, e, in);
     T* s = in.s;
     if constexpr (!is_f64<T>()) prewrap(s);
@@ -305,8 +322,8 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
 // thread hide latency at half the registers of two threads.
 template <bool TRACK, int SLOT>
 __device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e1, int li0,
-                                          int li1, EnvIn<float, TRACK>& in0,
-                                          EnvIn<float, TRACK>& in1, const void* act0,
+                                          int li1, EnvIn<float, TRACK, false>& in0,
+                                          EnvIn<float, TRACK, false>& in1, const void* act0,
                                           const void* act1, bool io_f64, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
                                           int8_t* __restrict__ reason, StatAcc& st) {
@@ -349,7 +366,7 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
                                           const void* __restrict__ act, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
                                           int8_t* __restrict__ reason, StatAcc& st) {
-    EnvIn<float, TRACK> in0, in1;
+    EnvIn<float, TRACK, false> in0, in1;
     load_env<float, TRACK>(p, e0, in0);
     load_env<float, TRACK>(p, e1, in1);
     pair_core<TRACK, SLOT>(p, e0, e1, li0, li1, in0, in1, act_row(p, act, e0),
