@@ -436,6 +436,15 @@ def main():
                           "fp32_frac": fl2 * e2.num_envs / ks / 1e12 / fp32_peak,
                           "hbm_frac": b2 * e2.num_envs / ks / 1e9 / hbm_peak,
                           "registers": e2.info["step_kernel_registers"]})
+            if name == "c5":   # the kernel at the size where it is throughput-bound
+                ach = fl2 * e2.num_envs / ks / 1e12
+                line["roofline_at_scale"] = {
+                    "config": name, "bound": "fp32", "achieved": ach, "peak": fp32_peak,
+                    "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                    "traffic": profile_traffic(name), "flops_per_env_step": fl2,
+                    "hbm": {"achieved": b2 * e2.num_envs / ks / 1e9, "peak": hbm_peak,
+                            "unit": "GB/s", "frac": b2 * e2.num_envs / ks / 1e9 / hbm_peak,
+                            "bytes_per_env_step": b2}}
             del e2, a2
             torch.cuda.empty_cache()
         line["sweep"] = sweep
