@@ -104,6 +104,14 @@ int32_t uuvsim_dev_reset(uint64_t handle, uint64_t seed, void* obs, uint64_t obs
                          uint64_t stream);
 int32_t uuvsim_dev_observe(uint64_t handle, void* obs, uint64_t obs_len, uint64_t stream);
 int32_t uuvsim_dev_bench_actions(uint64_t handle, void* actions, uint64_t len, uint64_t stream);
+/* exact slab checkpoint (no reference counterpart: its RNG counters are private,
+ * engine.rs:338-339).  uuvsim_snapshot_size -> bytes; uuvsim_snapshot fills a
+ * caller buffer of exactly that size; uuvsim_restore loads it into an engine of
+ * the same configuration (code 1 on a mismatch), after which steps continue
+ * bit-for-bit as in the engine that was saved. */
+int32_t uuvsim_snapshot_size(uint64_t handle, uint64_t* out_bytes);
+int32_t uuvsim_snapshot(uint64_t handle, void* buf, uint64_t len);
+int32_t uuvsim_restore(uint64_t handle, const void* buf, uint64_t len);
 /* register (buf != NULL) or clear (NULL) a caller-owned device buffer
  * [M][obs_dim] (engine precision): later device-face steps write each finished
  * env's TERMINAL observation (pre-reset state, terminating step) into its row;

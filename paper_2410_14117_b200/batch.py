@@ -295,6 +295,23 @@ class B200EnvBatch:
             self._handle, t["obs"].data_ptr(), t["obs"].numel(), self._stream(stream)))
         return t["obs"]
 
+    def snapshot(self) -> bytes:
+        """Exact checkpoint of the slab (states, counters, RNG counters, DR records)."""
+        self._require_open()
+        n = ctypes.c_uint64(0)
+        _core.check(self._lib, self._lib.uuvsim_snapshot_size(self._handle, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _core.check(self._lib, self._lib.uuvsim_snapshot(self._handle, buf, n.value))
+        return buf.raw
+
+    def restore(self, blob: bytes) -> None:
+        """Load a snapshot taken from an engine of the same configuration; the
+        next steps continue bit-for-bit.  Returns no observation (call
+        ``observe_tensors`` or step)."""
+        self._require_open()
+        _core.check(self._lib, self._lib.uuvsim_restore(self._handle, blob, len(blob)))
+        self.root_seed = int.from_bytes(blob[32:40], "little")   # SnapHeader.root_seed
+
     def states_tensor(self, out=None, stream=None):
         """Raw states [M, 12] on the device (engine precision), e.g. for PD control."""
         import torch

@@ -291,6 +291,31 @@ int32_t uuvsim_dev_states(uint64_t h, void* out, uint64_t len, uint64_t stream) 
     });
 }
 
+int32_t uuvsim_snapshot_size(uint64_t h, uint64_t* out) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        if (!out) return bad_size("snapshot size", 1, "u64");
+        *out = (uint64_t)e.snapshot_bytes();
+        return UUVSIM_OK;
+    });
+}
+
+int32_t uuvsim_snapshot(uint64_t h, void* buf, uint64_t len) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t want = (uint64_t)e.snapshot_bytes();
+        if (!buf || len != want) return bad_size("snapshot", want, "u8");
+        e.snapshot(buf);
+        return UUVSIM_OK;
+    });
+}
+
+int32_t uuvsim_restore(uint64_t h, const void* buf, uint64_t len) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        if (!buf) return bad_size("snapshot", (uint64_t)e.snapshot_bytes(), "u8");
+        e.restore(buf, (size_t)len);
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_set_final_obs(uint64_t h, void* buf, uint64_t len) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();

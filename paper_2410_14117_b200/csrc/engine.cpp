@@ -498,6 +498,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
         p.dr2 = (V2<T>*)carve(N * sizeof(V2<T>));
     }
     if (off > arena_bytes_) throw RuntimeError("internal: arena too small");
+    arena_used_ = off;
 }
 
 // Structure test for the PatFossen kernels (uuv_model.cuh): every entry outside
@@ -920,6 +921,82 @@ void Engine::dr_factors_host(double* out) {
     else cuda_check(Launch<float>::pack_dr(*pf_, d_pack_, stream_), "pack_dr");
     cuda_check(cudaMemcpyAsync(out, d_pack_, (size_t)m_ * 10 * 8, cudaMemcpyDeviceToHost, stream_), "dr D2H");
     cuda_check(cudaStreamSynchronize(stream_), "dr sync");
+}
+
+// ------------------------------------------------------------------ checkpoint
+namespace {
+struct SnapHeader {
+    char magic[8];            // "UUVB200S"
+    uint32_t version, precision_bytes;
+    uint64_t n_env, env_offset, root_seed, payload_bytes, config_hash;
+    uint32_t obs_dim, act_dim, dr, pad;
+};
+static_assert(sizeof(SnapHeader) == 72, "snapshot header layout");
+constexpr uint32_t kSnapVersion = 1;
+
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char* c = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    return h;
+}
+}  // namespace
+
+// fingerprint of everything that determines the dynamics and the draws: the
+// kernel parameter block minus buffer pointers and the per-launch root seed
+template <class T> static uint64_t hash_params(const EngineP<T>& p) {
+    uint64_t h = fnv1a(p.veh, sizeof(p.veh));
+    TaskP<T> tk = p.task;
+    tk.traj = nullptr;
+    h = fnv1a(&tk, sizeof(tk), h);
+    h = fnv1a(&p.ranges, sizeof(p.ranges), h);
+    h = fnv1a(&p.mix_bound0, sizeof(p.mix_bound0), h);
+    h = fnv1a(&p.n_veh, sizeof(p.n_veh), h);
+    return h;
+}
+
+uint64_t Engine::config_hash() const { return fp64_ ? hash_params(*pd_) : hash_params(*pf_); }
+
+size_t Engine::snapshot_bytes() const { return sizeof(SnapHeader) + arena_used_; }
+
+void Engine::snapshot(void* out) {
+    activate();
+    cuda_check(cudaStreamSynchronize(stream_), "snapshot sync");
+    cuda_check(cudaDeviceSynchronize(), "snapshot sync");   // device-face work on other streams
+    SnapHeader h{};
+    std::memcpy(h.magic, "UUVB200S", 8);
+    h.version = kSnapVersion;
+    h.precision_bytes = fp64_ ? 8 : 4;
+    h.n_env = (uint64_t)m_;
+    h.env_offset = env_offset_;
+    h.root_seed = fp64_ ? pd_->seed : pf_->seed;
+    h.payload_bytes = arena_used_;
+    h.config_hash = config_hash();
+    h.obs_dim = (uint32_t)obs_dim_;
+    h.act_dim = (uint32_t)n_act_;
+    h.dr = ranges_.enabled ? 1 : 0;
+    std::memcpy(out, &h, sizeof(h));
+    cuda_check(cudaMemcpy(static_cast<char*>(out) + sizeof(h), arena_, arena_used_,
+                          cudaMemcpyDeviceToHost), "snapshot D2H");
+}
+
+void Engine::restore(const void* in, size_t len) {
+    activate();
+    SnapHeader h{};
+    if (len < sizeof(h)) throw ConfigError("snapshot is truncated");
+    std::memcpy(&h, in, sizeof(h));
+    if (std::memcmp(h.magic, "UUVB200S", 8) != 0 || h.version != kSnapVersion)
+        throw ConfigError("not a B200 engine snapshot (bad magic or version)");
+    if (h.precision_bytes != (fp64_ ? 8u : 4u) || h.n_env != (uint64_t)m_ ||
+        h.env_offset != env_offset_ || h.obs_dim != (uint32_t)obs_dim_ ||
+        h.act_dim != (uint32_t)n_act_ || h.dr != (ranges_.enabled ? 1u : 0u) ||
+        h.payload_bytes != arena_used_ || h.config_hash != config_hash())
+        throw ConfigError("snapshot does not match this engine's configuration");
+    if (len != sizeof(h) + arena_used_) throw ConfigError("snapshot is truncated");
+    cuda_check(cudaDeviceSynchronize(), "restore sync");
+    cuda_check(cudaMemcpy(arena_, static_cast<const char*>(in) + sizeof(h), arena_used_,
+                          cudaMemcpyHostToDevice), "restore H2D");
+    if (fp64_) pd_->seed = h.root_seed;
+    else pf_->seed = h.root_seed;
 }
 
 void Engine::stats_host(double* out, bool clear) {

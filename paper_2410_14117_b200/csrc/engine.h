@@ -81,6 +81,13 @@ public:
     void dr_factors_host(double* out);     // [M][10]
     void stats_host(double* out, bool clear);
 
+    // exact slab checkpoint: header + the per-env device state (states, step
+    // counters, running returns, RNG counters, DR records, root seed).  Restoring
+    // into an engine of the same configuration continues bit-for-bit.
+    size_t snapshot_bytes() const;
+    void snapshot(void* out);
+    void restore(const void* in, size_t len);
+
     // device face (zero-copy, stream-ordered, graph-capturable).  Element type of
     // act/obs/rew is the engine precision: f32 for fp32 engines, f64 for fp64.
     bool is_fp64() const { return fp64_; }
@@ -139,6 +146,8 @@ private:
     // device memory
     void* arena_ = nullptr;
     size_t arena_bytes_ = 0;
+    size_t arena_used_ = 0;   // per-env state occupies arena_[0, arena_used_)
+    uint64_t config_hash() const;
     void* traj_ = nullptr;
     double* stats_part_ = nullptr;
     int nblk_ = 0;
