@@ -94,6 +94,33 @@ def build_config(name: str, rank: int, precision: str, pair: str = "auto",
     return cfg, [v.n_thrusters() for v in vdocs]
 
 
+def c4_loop(env, horizon: int = 64, reps: int = 5) -> dict:
+    """C4 rollout loop: normalise -> 2x64 tanh actor-critic -> Gaussian sample ->
+    clamp -> fused env step -> rollout buffers, one CUDA graph per horizon
+    (paper_2410_14117_b200.rollout).  Device time of `reps` graph replays."""
+    import torch
+
+    from paper_2410_14117_b200 import rollout as R
+    cfg = R.TrainConfig(num_envs=env.num_envs, horizon=horizon)
+    pol = R.ActorCritic(env.obs_dim, env.action_dim, seed=0).cuda()
+    norm = R.RunningNorm(env.obs_dim, "cuda")
+    ro = R.Rollout(env, pol, norm, cfg, use_graph=True)
+    ro.reset(0)
+    ro.collect()                       # warm-up + capture + first replay
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        ro.collect()
+    b.record()
+    torch.cuda.synchronize()
+    s = a.elapsed_time(b) / 1e3
+    return {"env_steps_per_sec": env.num_envs * horizon * reps / s,
+            "us_per_env_step_batch": s / (horizon * reps) * 1e6, "horizon": horizon,
+            "what": "policy (2x64 tanh actor-critic) + sampling + fused step + buffers, "
+                    "one CUDA graph per horizon"}
+
+
 def rank_device() -> int:
     return int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -436,6 +463,8 @@ def main():
                           "fp32_frac": fl2 * e2.num_envs / ks / 1e12 / fp32_peak,
                           "hbm_frac": b2 * e2.num_envs / ks / 1e9 / hbm_peak,
                           "registers": e2.info["step_kernel_registers"]})
+            if name == "c4":   # env-only and policy+env loop throughput
+                sweep[-1]["loop"] = c4_loop(e2)
             if name == "c5":   # the kernel at the size where it is throughput-bound
                 ach = fl2 * e2.num_envs / ks / 1e12
                 line["roofline_at_scale"] = {
