@@ -64,6 +64,9 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
         "uuvsim_dev_graph_capture": (i32, [u64, vp, vp, vp, vp, vp, u32]),
         "uuvsim_dev_graph_launch": (i32, [u64, u64]),
         "uuvsim_synchronize": (i32, [u64]),
+        "uuvsim_rl_policy_blocks": (u32, [u64]),
+        "uuvsim_rl_policy_act": (i32, [vp, u64]),
+        "uuvsim_rl_post": (i32, [vp, u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)   # AttributeError on a missing export, like the reference

@@ -142,7 +142,7 @@ class Rollout:
     """Horizon buffers + the graph-captured collection loop for one env slab."""
 
     def __init__(self, env, policy: ActorCritic, norm: RunningNorm, cfg: TrainConfig,
-                 use_graph: bool = True):
+                 use_graph: bool = True, fused: bool | None = None):
         self.env, self.policy, self.norm, self.cfg = env, policy, norm, cfg
         dev = torch.device("cuda", env.device_index)
         T, M = cfg.horizon, env.num_envs
@@ -158,12 +158,26 @@ class Rollout:
         self.boot_value = torch.zeros(M, device=dev, dtype=f)
         self.graph = None
         self.use_graph = use_graph
+        # fused path (csrc/rl_kernels.cu): policy + sampling + normaliser in one kernel
+        # and one small post kernel around each env step, instead of ~40 framework kernels
+        if fused is None:
+            fused = env.obs_dim <= 36 and env.action_dim <= 8 and policy.a1.weight.shape[0] == 64
+        self.fused = None
+        if fused:
+            from .rl_fused import FusedActorCritic
+            self.fused = FusedActorCritic(policy, norm, M, seed=cfg.seed + 7,
+                                          env_offset=getattr(env, "env_offset", 0))
+        self.env_obs = None
 
     def reset(self, seed: int):
-        self.obs.copy_(self.env.reset_tensors(seed))
+        self.env_obs = self.env.reset_tensors(seed)
+        self.obs.copy_(self.env_obs)
 
     @torch.no_grad()
     def _collect(self):
+        if self.fused is not None:
+            self._collect_fused()
+            return
         pol, norm, env = self.policy, self.norm, self.env
         std = torch.exp(pol.log_std)
         for t in range(self.cfg.horizon):
@@ -181,6 +195,18 @@ class Rollout:
             self.done_buf[t].copy_(d)
             self.obs.copy_(o)
         self.boot_value.copy_(pol(norm.normalize(self.obs))[1])
+
+    @torch.no_grad()
+    def _collect_fused(self):
+        F, env = self.fused, self.env
+        obs = self.env_obs
+        for t in range(self.cfg.horizon):
+            F.act(obs, nobs=self.obs_buf[t], raw=self.act_buf[t], act=self.act_in,
+                  logp=self.logp_buf[t], value=self.val_buf[t])
+            obs, r, d, _ = env.step_tensors(self.act_in)
+            F.post(r, d, self.rew_buf[t], self.done_buf[t])
+        F.act(obs, value=self.boot_value, sample=False, update_norm=False, value_only=True)
+        self.env_obs = obs
 
     def collect(self):
         """One horizon; the first call with use_graph captures it as a CUDA graph."""
@@ -264,7 +290,8 @@ def evaluate(policy: ActorCritic, norm: RunningNorm, make_env, episodes: int, se
 
 
 def train(make_env, cfg: TrainConfig, use_graph: bool = True, log_cb=None,
-          eval_every: int = 0, eval_episodes: int = 256, episode_len: int = 600) -> dict:
+          eval_every: int = 0, eval_episodes: int = 256, episode_len: int = 600,
+          fused: bool | None = None) -> dict:
     """collect -> GAE -> PPO update until cfg.total_env_steps (ppo.py:245-338)."""
     env = make_env(cfg.num_envs, cfg.seed)
     dev = torch.device("cuda", env.device_index)
@@ -274,7 +301,7 @@ def train(make_env, cfg: TrainConfig, use_graph: bool = True, log_cb=None,
     norm = RunningNorm(env.obs_dim, dev)
     torch.manual_seed(cfg.seed + 1)
     gen = torch.Generator(device=dev).manual_seed(cfg.seed + 2)
-    ro = Rollout(env, policy, norm, cfg, use_graph)
+    ro = Rollout(env, policy, norm, cfg, use_graph, fused=fused)
     ro.reset(cfg.seed)
     env_steps, it = 0, 0
     t_collect = t_update = 0.0

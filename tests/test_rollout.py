@@ -127,3 +127,102 @@ def test_short_training_reduces_station_error():
     assert np.isfinite(out["metrics"][-1]["loss"])
     assert after["mean_pos_err_m"] < 0.8 * before["mean_pos_err_m"], (before, after)
     assert out["collect_env_steps_per_sec"] > 2e6
+
+
+# ---------------------------------------------------------------- fused kernels ---
+
+def _random_policy(obs_dim, act_dim, seed):
+    pol = R.ActorCritic(obs_dim, act_dim, seed=seed).cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    with torch.no_grad():
+        for prm in pol.parameters():     # non-trivial biases / weights / log-std
+            prm.add_(0.1 * torch.randn(prm.shape, device="cuda", generator=g))
+    return pol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("obs_dim,act_dim", [(12, 6), (36, 8), (24, 6)])
+def test_fused_policy_matches_torch(obs_dim, act_dim):
+    from paper_2410_14117_b200.rl_fused import FusedActorCritic
+    M = 1000
+    pol = _random_policy(obs_dim, act_dim, 3)
+    norm = R.RunningNorm(obs_dim, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    norm.mean.copy_(torch.randn(obs_dim, device="cuda", generator=g, dtype=torch.float64))
+    norm.var.copy_(torch.rand(obs_dim, device="cuda", generator=g, dtype=torch.float64) + 0.1)
+    norm.count.fill_(123.0)
+    obs = 3.0 * torch.randn((M, obs_dim), device="cuda", generator=g)
+    ref_norm = R.RunningNorm(obs_dim, "cuda")
+    ref_norm.mean.copy_(norm.mean); ref_norm.var.copy_(norm.var); ref_norm.count.copy_(norm.count)
+    F = FusedActorCritic(pol, norm, M)
+    nobs = torch.empty((M, obs_dim), device="cuda")
+    raw = torch.empty((M, act_dim), device="cuda")
+    act = torch.empty_like(raw)
+    logp = torch.empty(M, device="cuda")
+    value = torch.empty(M, device="cuda")
+    F.act(obs, nobs=nobs, raw=raw, act=act, logp=logp, value=value, sample=False)
+    F.post()
+    torch.cuda.synchronize()
+    with torch.no_grad():
+        want_nobs = ref_norm.normalize(obs)
+        mean, v = pol(want_nobs)
+        want_logp = pol.log_prob(mean, mean)
+    ref_norm.update(obs)
+    torch.testing.assert_close(nobs, want_nobs, rtol=1e-6, atol=1e-6)
+    torch.testing.assert_close(raw, mean, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(act, mean.clamp(-1, 1), rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(value, v, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(logp, want_logp, rtol=1e-6, atol=1e-5)
+    torch.testing.assert_close(norm.mean, ref_norm.mean, rtol=1e-10, atol=1e-12)
+    torch.testing.assert_close(norm.var, ref_norm.var, rtol=1e-9, atol=1e-12)
+    torch.testing.assert_close(norm.count, ref_norm.count)
+    assert int(F.noise_ctr.item()) == 1
+
+
+@pytest.mark.gpu
+def test_fused_noise_is_standard_normal_and_logp_consistent():
+    from paper_2410_14117_b200.rl_fused import FusedActorCritic
+    M, D, A = 16384, 12, 6
+    pol = _random_policy(D, A, 1)
+    with torch.no_grad():
+        pol.log_std.zero_()
+    norm = R.RunningNorm(D, "cuda")
+    F = FusedActorCritic(pol, norm, M, seed=11)
+    obs = torch.randn((M, D), device="cuda")
+    raw = torch.empty((M, A), device="cuda")
+    raw2 = torch.empty_like(raw)
+    logp = torch.empty(M, device="cuda")
+    F.act(obs, raw=raw, logp=logp, update_norm=False)
+    F.post(update_norm=False)
+    F.act(obs, raw=raw2, update_norm=False)
+    torch.cuda.synchronize()
+    with torch.no_grad():
+        mean, _ = pol(norm.normalize(obs))
+        eps = (raw - mean).double()
+        want_logp = pol.log_prob(raw, mean)
+    assert abs(float(eps.mean())) < 0.01
+    assert 0.97 < float(eps.var()) < 1.03
+    assert abs(float((eps ** 3).mean())) < 0.05            # symmetric
+    assert 2.85 < float((eps ** 4).mean()) < 3.15           # Gaussian kurtosis
+    torch.testing.assert_close(logp, want_logp, rtol=1e-5, atol=1e-4)
+    assert not torch.equal(raw, raw2)                       # the counter advanced
+
+
+@pytest.mark.gpu
+def test_fused_collect_matches_framework_collect():
+    make = _make_env("circle")
+    cfg = R.TrainConfig(num_envs=2048, horizon=16, init_log_std=-40.0)
+    outs = []
+    for fused in (False, True):
+        env = make(cfg.num_envs, 3)
+        pol = R.ActorCritic(env.obs_dim, env.action_dim, seed=1, init_log_std=-40.0).cuda()
+        norm = R.RunningNorm(env.obs_dim, "cuda")
+        ro = R.Rollout(env, pol, norm, cfg, use_graph=False, fused=fused)
+        ro.reset(3)
+        ro.collect()
+        torch.cuda.synchronize()
+        outs.append([b.clone() for b in (ro.obs_buf, ro.rew_buf, ro.done_buf, ro.val_buf,
+                                         ro.boot_value, norm.mean, norm.var)])
+        env.close()
+    for a, b in zip(*outs):
+        torch.testing.assert_close(a.double(), b.double(), rtol=1e-4, atol=1e-4)

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--dr", action="store_true")
     ap.add_argument("--eval-every", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="framework-op policy path")
     a = ap.parse_args()
     base = uuv.bluerov2_params() if a.vehicle == "bluerov2" else uuv.default_params()
 
@@ -46,7 +47,8 @@ def main():
                         minibatch=a.minibatch, epochs=a.epochs, lr=a.lr)
     t0 = time.perf_counter()
     out = R.train(make, cfg, use_graph=not a.no_graph, eval_every=a.eval_every,
-                  log_cb=lambda r: print(json.dumps(r), flush=True))
+                  log_cb=lambda r: print(json.dumps(r), flush=True),
+                  fused=False if a.unfused else None)
     wall = time.perf_counter() - t0
     final = R.evaluate(out["policy"], out["normalizer"], make, 1024, 1000, 600)
     print(json.dumps({"summary": True, "task": a.task, "envs": a.envs, "env_steps": out["env_steps"],
