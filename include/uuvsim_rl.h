@@ -11,6 +11,9 @@
  *                         head, linear value head; nets.py:31-55), Gaussian sample
  *                         with a state-independent log-std, clamp, log-prob, and
  *                         per-block partial sums for the normaliser update
+ *   (the policy layers run on the 5th-generation tensor cores -- tcgen05.mma
+ *   kind::tf32, 3xTF32 split for fp32 accuracy, accumulators in TMEM -- when a
+ *   weight image from uuvsim_rl_prepare is passed; else on the CUDA cores)
  *   uuvsim_rl_post        merge the partial sums into mean/var/count (parallel
  *                         variance formula, nets.py:177-188), copy reward / done
  *                         into the rollout buffers, advance the noise counter
@@ -51,7 +54,9 @@ typedef struct {
     float* act_out;          /* [M][A] clamped to [-1, 1] (the env's action tensor), or NULL */
     float* logp_out;         /* [M], or NULL */
     float* value_out;        /* [M], or NULL */
-    double* stats_part;      /* [grid][2 D] (sum x, sum x^2) per block when flags & 2 */
+    double* stats_part;      /* [uuvsim_rl_policy_blocks(M)][2 D] (sum x, sum x^2) when flags & 2 */
+    const void* wimage;      /* tensor-core weight image from uuvsim_rl_prepare, or NULL
+                                (then the CUDA-core kernel runs) */
 } UuvRlPolicyArgs;
 
 typedef struct {
@@ -71,6 +76,12 @@ typedef struct {
 
 /* partial rows the policy launch writes for num_envs (size of stats_part / (2 D)) */
 uint32_t uuvsim_rl_policy_blocks(uint64_t num_envs);
+/* bytes of the tensor-core weight image for obs_dim (multiple of 16) */
+uint64_t uuvsim_rl_image_bytes(uint32_t obs_dim);
+/* build the weight image (3xTF32 hi/lo splits in the UMMA K-major core-matrix
+ * layout + biases/heads) from the parameter pointers in args; run it whenever the
+ * parameters change (once per collected horizon) */
+int32_t uuvsim_rl_prepare(const UuvRlPolicyArgs* args, void* image, uint64_t len, uint64_t stream);
 int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* args, uint64_t stream);
 int32_t uuvsim_rl_post(const UuvRlPostArgs* args, uint64_t stream);
 

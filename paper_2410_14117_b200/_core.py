@@ -67,6 +67,8 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
         "uuvsim_rl_policy_blocks": (u32, [u64]),
         "uuvsim_rl_policy_act": (i32, [vp, u64]),
         "uuvsim_rl_post": (i32, [vp, u64]),
+        "uuvsim_rl_image_bytes": (u64, [u32]),
+        "uuvsim_rl_prepare": (i32, [vp, vp, u64, u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)   # AttributeError on a missing export, like the reference

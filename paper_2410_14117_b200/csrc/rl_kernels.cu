@@ -310,10 +310,439 @@ template <int DP> static cudaError_t launch_policy(const UuvRlPolicyArgs& a, cud
 
 }  // namespace uuvrl
 
+// ============================================================================
+// Tensor-core policy kernel (tcgen05, sm_100a).
+//
+// A CTA holds M = 128 envs = one UMMA tile row block.  Every dense layer of both
+// trunks is D[128 x 64] = A[128 x K] B[64 x K]^T on the 5th-generation tensor
+// cores: A (normalised obs, then hidden activations) and B (weights) sit in
+// shared memory in the K-major, no-swizzle UMMA core-matrix layout (8 rows x 16 B
+// per core matrix), the fp32 accumulator in TMEM (64 columns), and one elected
+// thread issues kind::tf32 MMAs, K = 8 per instruction.  fp32 accuracy comes from
+// the 3xTF32 split: x = x_hi + x_lo with x_hi = tf32(x), and
+// A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi (error ~1e-7 relative, vs ~5e-4 for
+// one TF32 pass).  The weights are split and laid out once per parameter update
+// by k_rl_prepare into a global "image" that each CTA pulls into shared memory
+// with ONE cp.async.bulk while it normalises its observations.  Epilogues: one
+// thread per env reads its TMEM row (tcgen05.ld 32x32b), adds the bias, applies
+// tanh and writes the next layer's A operand (hi/lo) back to shared memory; the
+// scalar heads (value, 8 action means), sampling and log-prob stay on the CUDA
+// cores as in the FFMA kernel.
+// ============================================================================
+namespace uuvtc {
+
+constexpr int M = 128, H = 64, AMAX = 8;
+constexpr uint32_t IDESC_TF32 = (1u << 4)      // D format f32
+                              | (2u << 7)      // A format tf32
+                              | (2u << 10)     // B format tf32
+                              | ((uint32_t)(H >> 3) << 17)    // N = 64
+                              | ((uint32_t)(M >> 4) << 24);   // M = 128
+// small-parameter block (floats) at the end of the image
+constexpr int S_B1C = 0, S_B2C = 64, S_CV = 128, S_CVB = 192, S_B1A = 196, S_B2A = 260,
+              S_AM = 324, S_AMB = 836, S_LS = 844, S_N = 852;
+
+__host__ __device__ constexpr int k1p(int D) { return (D + 7) / 8 * 8; }
+struct Img {
+    uint32_t k1, w1c_hi, w1c_lo, w2c_hi, w2c_lo, w1a_hi, w1a_lo, w2a_hi, w2a_lo, small, total;
+};
+__host__ __device__ inline Img img_layout(int D) {
+    Img g{};
+    g.k1 = (uint32_t)k1p(D);
+    const uint32_t m1 = H * g.k1 * 4, m2 = H * H * 4;
+    uint32_t o = 0;
+    g.w1c_hi = o; o += m1; g.w1c_lo = o; o += m1; g.w2c_hi = o; o += m2; g.w2c_lo = o; o += m2;
+    g.w1a_hi = o; o += m1; g.w1a_lo = o; o += m1; g.w2a_hi = o; o += m2; g.w2a_lo = o; o += m2;
+    g.small = o;
+    o += S_N * 4;
+    g.total = (o + 15) / 16 * 16;
+    return g;
+}
+// byte offset of element (row, k) in a K-major core-matrix tile with KC = K / 4
+__host__ __device__ inline uint32_t cm_off(int row, int k, int KC) {
+    return (uint32_t)((((row >> 3) * KC + (k >> 2)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
+}
+
+__device__ __forceinline__ float tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// UMMA shared-memory descriptor: K-major, SWIZZLE_NONE, LBO = 128 B (next K
+// core matrix), SBO = KC * 128 B (next 8-row group), version 1 (sm_100)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, int KC) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((128u >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)(((uint32_t)KC * 128u >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(IDESC_TF32), "r"(acc));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n"
+        "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra W_%=;\n}" ::"r"(s_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// weight image: hi/lo tf32 splits in the core-matrix layout + the small block
+__global__ void k_rl_prepare(const UuvRlPolicyArgs a, unsigned char* img) {
+    const Img g = img_layout((int)a.obs_dim);
+    const int D = (int)a.obs_dim, A = (int)a.act_dim, K1 = (int)g.k1;
+    const int n1 = H * K1, n2 = H * H;
+    const int total = 2 * n1 + 2 * n2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const float* W;
+        int K, KIN, j = i;
+        uint32_t hi_off, lo_off;
+        if (j < n1) { W = a.c1w; K = K1; KIN = D; hi_off = g.w1c_hi; lo_off = g.w1c_lo; }
+        else if ((j -= n1) < n2) { W = a.c2w; K = H; KIN = H; hi_off = g.w2c_hi; lo_off = g.w2c_lo; }
+        else if ((j -= n2) < n1) { W = a.a1w; K = K1; KIN = D; hi_off = g.w1a_hi; lo_off = g.w1a_lo; }
+        else { j -= n1; W = a.a2w; K = H; KIN = H; hi_off = g.w2a_hi; lo_off = g.w2a_lo; }
+        const int n = j / K, k = j - n * K;
+        const float w = k < KIN ? W[n * KIN + k] : 0.0f;
+        const float hi = tf32(w);
+        const uint32_t o = cm_off(n, k, K / 4);
+        *reinterpret_cast<float*>(img + hi_off + o) = hi;
+        *reinterpret_cast<float*>(img + lo_off + o) = tf32(w - hi);
+    }
+    float* sp = reinterpret_cast<float*>(img + g.small);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S_N; i += gridDim.x * blockDim.x) {
+        float v = 0.0f;
+        if (i < S_B2C) v = a.c1b[i];
+        else if (i < S_CV) v = a.c2b[i - S_B2C];
+        else if (i < S_CVB) v = a.cvw[i - S_CV];
+        else if (i < S_B1A) v = i == S_CVB ? a.cvb[0] : 0.0f;
+        else if (i < S_B2A) v = a.a1b[i - S_B1A];
+        else if (i < S_AM) v = a.a2b[i - S_B2A];
+        else if (i < S_AMB) { const int r = (i - S_AM) / H; v = r < A ? a.amw[i - S_AM] : 0.0f; }
+        else if (i < S_LS) { const int r = i - S_AMB; v = r < A ? a.amb[r] : 0.0f; }
+        else { const int r = i - S_LS; v = r < A ? a.log_std[r] : 0.0f; }
+        sp[i] = v;
+    }
+}
+
+// epilogue of a hidden layer for 32 of this env's units (column half ch):
+// tanh(acc + b) -> next layer's A operand (hi/lo)
+__device__ __forceinline__ void epi_hidden(uint32_t tacc, const float* b, unsigned char* a_hi,
+                                           unsigned char* a_lo, int row, int ch) {
+#pragma unroll 1   // compact code: the CTA's warps run in near lockstep, an icache miss stalls all
+    for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+        float v[16];
+        tmem_ld16(tacc + 16 * c16, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float4 hi, lo;
+            float* hp = &hi.x;
+            float* lp = &lo.x;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int j = 16 * c16 + 4 * q + t;
+                const float x = tanhf(v[4 * q + t] + b[j]);
+                hp[t] = tf32(x);
+                lp[t] = tf32(x - hp[t]);
+            }
+            const uint32_t o = cm_off(row, 16 * c16 + 4 * q, H / 4);
+            *reinterpret_cast<float4*>(a_hi + o) = hi;
+            *reinterpret_cast<float4*>(a_lo + o) = lo;
+        }
+    }
+}
+
+// one layer: D(tmem) = A B^T with 3xTF32, K = kdim; commit to bar
+__device__ __forceinline__ void issue_layer(uint32_t tmem, const unsigned char* a_hi,
+                                            const unsigned char* a_lo, const unsigned char* b_hi,
+                                            const unsigned char* b_lo, int kdim, uint64_t* bar) {
+    const int KC = kdim / 4;
+    const uint32_t ah = s_u32(a_hi), al = s_u32(a_lo), bh = s_u32(b_hi), bl = s_u32(b_lo);
+    for (int ks = 0; ks < kdim / 8; ++ks) {   // K = 8 per MMA: two core matrices along K
+        const uint32_t off = ks * 256u;
+        mma_tf32(tmem, umma_desc(ah + off, KC), umma_desc(bh + off, KC), ks > 0 ? 1u : 0u);
+        mma_tf32(tmem, umma_desc(ah + off, KC), umma_desc(bl + off, KC), 1u);
+        mma_tf32(tmem, umma_desc(al + off, KC), umma_desc(bh + off, KC), 1u);
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(s_u32(bar)) : "memory");
+}
+
+constexpr int NT = 2 * M;   // threads: two per env (TMEM lane quarter = warp % 4, column half = warp / 4)
+
+__global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[2];   // [0] weights landed, [1] MMA done
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ double nsc[2 * 36];              // normaliser mean, 1 / sqrt(var + 1e-8)
+    __shared__ float red[2][M];                 // cross-half partials
+    const int D = (int)a.obs_dim, A = (int)a.act_dim;
+    const bool value_only = (a.flags & 4) != 0;
+    const Img g = img_layout(D);
+    const int K1 = (int)g.k1;
+    unsigned char* wimg = smem;                          // image copy
+    unsigned char* az_hi = smem + g.total;               // [128][K1] core-matrix
+    unsigned char* az_lo = az_hi + M * K1 * 4;
+    unsigned char* ah_hi = az_lo + M * K1 * 4;           // [128][64] core-matrix
+    unsigned char* ah_lo = ah_hi + M * H * 4;
+    const float* sp = reinterpret_cast<const float*>(wimg + g.small);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row = ((warp & 3) << 5) + lane;            // env in CTA = TMEM lane
+    const int ch = warp >> 2;                            // column half
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < D) {
+        nsc[tid] = a.norm_mean[tid];
+        nsc[36 + tid] = 1.0 / sqrt(a.norm_var[tid] + 1e-8);
+    }
+    __syncwarp();
+    if (warp == 0) {   // 64 TMEM columns: one fp32 128 x 64 accumulator
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;"
+                     ::"r"(s_u32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    if (tid == 0) {   // the whole weight image in one bulk copy
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(s_u32(&bars[0])), "r"(g.total) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(s_u32(wimg)), "l"(a.wimage), "r"(g.total), "r"(s_u32(&bars[0])) : "memory");
+    }
+
+    // ---- observations (column half 0): normaliser sums, normalise + clip, A_z, nobs_out
+    const uint64_t e = (uint64_t)blockIdx.x * M + row;
+    const bool active = e < a.num_envs;
+    float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][37] (A_h unused yet)
+    if (ch == 0) {
+#pragma unroll 4
+        for (int k = 0; k < D; ++k) raw[row * 37 + k] = active ? __ldg(a.obs + e * D + k) : 0.0f;
+    }
+    __syncthreads();
+    if ((a.flags & 2) && tid < 2 * D) {
+        const int d = tid < D ? tid : tid - D;
+        const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
+        const int nvalid = left < (uint64_t)M ? (int)left : M;
+        double acc = 0.0;
+        for (int r = 0; r < nvalid; ++r) {
+            const double v = raw[r * 37 + d];
+            acc += tid < D ? v : v * v;
+        }
+        const uint32_t row2 = 2u * blockIdx.x;
+        a.stats_part[(size_t)row2 * 2 * D + tid] = acc;
+        a.stats_part[(size_t)(row2 + 1) * 2 * D + tid] = 0.0;   // FFMA-kernel granularity
+    }
+    // normalise: the two column halves split the K chunks
+#pragma unroll 1
+    for (int k4 = ch; 4 * k4 < K1; k4 += 2) {
+        float4 hi, lo;
+        float* hp = &hi.x;
+        float* lp = &lo.x;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int k = 4 * k4 + t;
+            float zk = 0.0f;
+            if (k < D) {   // RunningNorm.normalize in fp64
+                double v = ((double)raw[row * 37 + k] - nsc[k]) * nsc[36 + k];
+                v = fmin(fmax(v, -a.norm_clip), a.norm_clip);
+                zk = (float)v;
+                if (active && a.nobs_out) a.nobs_out[e * D + k] = zk;
+            }
+            hp[t] = tf32(zk);
+            lp[t] = tf32(zk - hp[t]);
+        }
+        const uint32_t o = cm_off(row, 4 * k4, K1 / 4);
+        *reinterpret_cast<float4*>(az_hi + o) = hi;
+        *reinterpret_cast<float4*>(az_lo + o) = lo;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // A_z -> tensor-core proxy
+    __syncthreads();
+    mbar_wait(&bars[0], 0);                                        // weights landed
+    const uint32_t tacc = tmem + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lanes
+
+    // ---- critic: value = cv . tanh(W2c tanh(W1c z + b1c) + b2c) + cvb
+    if (tid == 0) {
+        tc_fence_after();
+        issue_layer(tmem, az_hi, az_lo, wimg + g.w1c_hi, wimg + g.w1c_lo, K1, &bars[1]);
+    }
+    mbar_wait(&bars[1], 0);
+    tc_fence_after();
+    epi_hidden(tacc, sp + S_B1C, ah_hi, ah_lo, row, ch);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        tc_fence_after();
+        issue_layer(tmem, ah_hi, ah_lo, wimg + g.w2c_hi, wimg + g.w2c_lo, H, &bars[1]);
+    }
+    mbar_wait(&bars[1], 1);
+    tc_fence_after();
+    {
+        float vp = 0.0f;
+#pragma unroll 1
+        for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+            float v[16];
+            tmem_ld16(tacc + 16 * c16, v);
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                vp = fmaf(sp[S_CV + 16 * c16 + t], tanhf(v[t] + sp[S_B2C + 16 * c16 + t]), vp);
+        }
+        red[ch][row] = vp;
+    }
+    // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
+    // the mean head; A_z's region is free once the actor's first layer has consumed it
+    float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;   // (after actor L2 only)
+    tc_fence_before();
+    __syncthreads();   // all TMEM reads of the critic done; red complete
+    const float value = red[0][row] + red[1][row] + sp[S_CVB];
+    if (!value_only) {
+        // ---- actor: mean = tanh(am tanh(W2a tanh(W1a z + b1a) + b2a) + amb)
+        if (tid == 0) {
+            tc_fence_after();
+            issue_layer(tmem, az_hi, az_lo, wimg + g.w1a_hi, wimg + g.w1a_lo, K1, &bars[1]);
+        }
+        mbar_wait(&bars[1], 0);
+        tc_fence_after();
+        epi_hidden(tacc, sp + S_B1A, ah_hi, ah_lo, row, ch);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            issue_layer(tmem, ah_hi, ah_lo, wimg + g.w2a_hi, wimg + g.w2a_lo, H, &bars[1]);
+        }
+        mbar_wait(&bars[1], 1);   // A_h consumed: hrow may overwrite it
+        tc_fence_after();
+#pragma unroll 1
+        for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+            float v[16];
+            tmem_ld16(tacc + 16 * c16, v);
+#pragma unroll
+            for (int t = 0; t < 16; t += 4)
+                *reinterpret_cast<float4*>(hrow + 16 * c16 + t) = make_float4(
+                    tanhf(v[t] + sp[S_B2A + 16 * c16 + t]), tanhf(v[t + 1] + sp[S_B2A + 16 * c16 + t + 1]),
+                    tanhf(v[t + 2] + sp[S_B2A + 16 * c16 + t + 2]),
+                    tanhf(v[t + 3] + sp[S_B2A + 16 * c16 + t + 3]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+    if (value_only) {
+        if (active && ch == 0 && a.value_out) a.value_out[e] = value;
+        return;
+    }
+    // action dims: half ch takes Box-Muller pairs 2 ch and 2 ch + 1 (dims 4 ch .. 4 ch + 3)
+    const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;
+    const uint64_t gid = a.env_offset + e;
+    float logp = 0.0f;
+#pragma unroll 1
+    for (int p = 2 * ch; p < 2 * ch + 2; ++p) {
+        if (2 * p >= A) break;
+        float eps0 = 0.0f, eps1 = 0.0f;
+        if (a.flags & 1) {   // Box-Muller on the counter-based stream
+            const uint64_t bits = uuv::draw_u64(a.seed, gid, 3, ctr * 4 + (uint64_t)p);
+            const float u1 = ((float)(uint32_t)(bits >> 40) + 0.5f) * 5.9604644775390625e-08f;
+            const float u2 = (float)(uint32_t)(bits & 0xffffffu) * 5.9604644775390625e-08f;
+            const float r = sqrtf(-2.0f * __logf(u1));
+            float sn, cs;
+            __sincosf(6.28318530717958647f * u2, &sn, &cs);
+            eps0 = r * cs;
+            eps1 = r * sn;
+        }
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+            const int i = 2 * p + q;
+            if (i >= A) break;
+            float c0 = sp[S_AMB + i], c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+            const float4* w4 = reinterpret_cast<const float4*>(sp + S_AM + i * H);
+            const float4* h4 = reinterpret_cast<const float4*>(hrow);
+#pragma unroll 4
+            for (int k = 0; k < H / 4; ++k) {
+                const float4 w = w4[k], hv = h4[k];
+                c0 = fmaf(w.x, hv.x, c0);
+                c1 = fmaf(w.y, hv.y, c1);
+                c2 = fmaf(w.z, hv.z, c2);
+                c3 = fmaf(w.w, hv.w, c3);
+            }
+            const float mean = tanhf((c0 + c1) + (c2 + c3));
+            const float lsd = sp[S_LS + i];
+            const float rawv = fmaf(expf(lsd), q ? eps1 : eps0, mean);
+            const float zz = (rawv - mean) * expf(-lsd);      // ActorCritic.log_prob
+            logp += -0.5f * zz * zz - lsd - 0.918938533204672742f;
+            if (active && a.raw_out) a.raw_out[e * A + i] = rawv;
+            if (active && a.act_out) a.act_out[e * A + i] = fminf(fmaxf(rawv, -1.0f), 1.0f);
+        }
+    }
+    red[ch][row] = logp;
+    __syncthreads();
+    if (active && ch == 0) {
+        if (a.logp_out) a.logp_out[e] = red[0][row] + red[1][row];
+        if (a.value_out) a.value_out[e] = value;
+    }
+}
+
+inline size_t smem_bytes(int D) {
+    const Img g = img_layout(D);
+    return (size_t)g.total + 2 * (size_t)M * g.k1 * 4 + 2 * (size_t)M * H * 4;
+}
+
+}  // namespace uuvtc
+
 extern "C" {
 
 uint32_t uuvsim_rl_policy_blocks(uint64_t num_envs) {
-    return (uint32_t)((num_envs + uuvrl::ENVS - 1) / uuvrl::ENVS);
+    // rows for both kernels: 64-env FFMA blocks, or two rows per 128-env tensor-core CTA
+    return (uint32_t)(2 * ((num_envs + uuvtc::M - 1) / uuvtc::M));
+}
+
+uint64_t uuvsim_rl_image_bytes(uint32_t obs_dim) {
+    return obs_dim == 0 || obs_dim > 36 ? 0 : uuvtc::img_layout((int)obs_dim).total;
+}
+
+int32_t uuvsim_rl_prepare(const UuvRlPolicyArgs* a, void* image, uint64_t len, uint64_t stream) {
+    if (!a || !image || a->obs_dim == 0 || a->obs_dim > 36 || a->act_dim == 0 ||
+        a->act_dim > uuvtc::AMAX || a->hidden != uuvtc::H ||
+        len != uuvtc::img_layout((int)a->obs_dim).total)
+        return 3;
+    uuvtc::k_rl_prepare<<<64, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        *a, static_cast<unsigned char*>(image));
+    return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* a, uint64_t stream) {
@@ -323,6 +752,18 @@ int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* a, uint64_t stream) {
         ((a->flags & 2) && !a->stats_part))
         return 3;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (a->wimage) {   // tensor cores
+        const size_t smem = uuvtc::smem_bytes((int)a->obs_dim);
+        static int max_set = 0;
+        if ((int)smem > max_set) {
+            cudaFuncSetAttribute(uuvtc::k_policy_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)uuvtc::smem_bytes(36));
+            max_set = (int)uuvtc::smem_bytes(36);
+        }
+        const unsigned grid = (unsigned)((a->num_envs + uuvtc::M - 1) / uuvtc::M);
+        uuvtc::k_policy_tc<<<grid, uuvtc::NT, smem, st>>>(*a);
+        return cudaGetLastError() == cudaSuccess ? 0 : 4;
+    }
     const cudaError_t e = a->obs_dim <= 12 ? uuvrl::launch_policy<12>(*a, st)
                                            : uuvrl::launch_policy<36>(*a, st);
     return e == cudaSuccess ? 0 : 4;

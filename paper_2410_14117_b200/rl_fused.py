@@ -30,7 +30,7 @@ class PolicyArgs(ctypes.Structure):
                 ("a1w", _f), ("a1b", _f), ("a2w", _f), ("a2b", _f), ("amw", _f), ("amb", _f),
                 ("c1w", _f), ("c1b", _f), ("c2w", _f), ("c2b", _f), ("cvw", _f), ("cvb", _f),
                 ("log_std", _f), ("nobs_out", _f), ("raw_out", _f), ("act_out", _f),
-                ("logp_out", _f), ("value_out", _f), ("stats_part", _f)]
+                ("logp_out", _f), ("value_out", _f), ("stats_part", _f), ("wimage", _f)]
 
 
 class PostArgs(ctypes.Structure):
@@ -48,7 +48,8 @@ def _p(t):
 
 
 class FusedActorCritic:
-    def __init__(self, policy, norm, num_envs: int, seed: int = 0, env_offset: int = 0):
+    def __init__(self, policy, norm, num_envs: int, seed: int = 0, env_offset: int = 0,
+                 tensor_cores: bool = True):
         self.lib = _core.load()
         self.policy, self.norm = policy, norm
         self.M = int(num_envs)
@@ -65,6 +66,11 @@ class FusedActorCritic:
         self.noise_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
         self.n_part = int(self.lib.uuvsim_rl_policy_blocks(self.M))
         self.stats_part = torch.zeros(self.n_part * 2 * self.D, dtype=torch.float64, device=dev)
+        # tcgen05 path: weights split to 3xTF32 in the UMMA layout by prepare()
+        self.image = None
+        if tensor_cores:
+            nb = int(self.lib.uuvsim_rl_image_bytes(self.D))
+            self.image = torch.zeros(nb, dtype=torch.uint8, device=dev)
 
     def _args(self, obs, flags, nobs=None, raw=None, act=None, logp=None, value=None):
         pol, nm = self.policy, self.norm
@@ -75,7 +81,17 @@ class FusedActorCritic:
             _p(pol.am.weight), _p(pol.am.bias), _p(pol.c1.weight), _p(pol.c1.bias),
             _p(pol.c2.weight), _p(pol.c2.bias), _p(pol.cv.weight), _p(pol.cv.bias),
             _p(pol.log_std), _p(nobs), _p(raw), _p(act), _p(logp), _p(value),
-            _p(self.stats_part))
+            _p(self.stats_part), _p(self.image))
+
+    def prepare(self):
+        """(Re)build the tensor-core weight image from the current parameters --
+        once per horizon (stream-ordered, graph-capturable)."""
+        if self.image is None:
+            return
+        a = self._args(None, 0)
+        _core.check(self.lib, self.lib.uuvsim_rl_prepare(
+            ctypes.byref(a), self.image.data_ptr(), self.image.numel(),
+            torch.cuda.current_stream().cuda_stream))
 
     def act(self, obs, nobs=None, raw=None, act=None, logp=None, value=None,
             sample: bool = True, update_norm: bool = True, value_only: bool = False):

@@ -200,6 +200,7 @@ class Rollout:
     def _collect_fused(self):
         F, env = self.fused, self.env
         obs = self.env_obs
+        F.prepare()   # parameters changed since the last horizon (PPO update)
         for t in range(self.cfg.horizon):
             F.act(obs, nobs=self.obs_buf[t], raw=self.act_buf[t], act=self.act_in,
                   logp=self.logp_buf[t], value=self.val_buf[t])

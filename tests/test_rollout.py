@@ -141,8 +141,9 @@ def _random_policy(obs_dim, act_dim, seed):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("tc", [False, True], ids=["cuda_cores", "tcgen05"])
 @pytest.mark.parametrize("obs_dim,act_dim", [(12, 6), (36, 8), (24, 6)])
-def test_fused_policy_matches_torch(obs_dim, act_dim):
+def test_fused_policy_matches_torch(obs_dim, act_dim, tc):
     from paper_2410_14117_b200.rl_fused import FusedActorCritic
     M = 1000
     pol = _random_policy(obs_dim, act_dim, 3)
@@ -154,7 +155,8 @@ def test_fused_policy_matches_torch(obs_dim, act_dim):
     obs = 3.0 * torch.randn((M, obs_dim), device="cuda", generator=g)
     ref_norm = R.RunningNorm(obs_dim, "cuda")
     ref_norm.mean.copy_(norm.mean); ref_norm.var.copy_(norm.var); ref_norm.count.copy_(norm.count)
-    F = FusedActorCritic(pol, norm, M)
+    F = FusedActorCritic(pol, norm, M, tensor_cores=tc)
+    F.prepare()
     nobs = torch.empty((M, obs_dim), device="cuda")
     raw = torch.empty((M, act_dim), device="cuda")
     act = torch.empty_like(raw)
@@ -188,6 +190,7 @@ def test_fused_noise_is_standard_normal_and_logp_consistent():
         pol.log_std.zero_()
     norm = R.RunningNorm(D, "cuda")
     F = FusedActorCritic(pol, norm, M, seed=11)
+    F.prepare()
     obs = torch.randn((M, D), device="cuda")
     raw = torch.empty((M, A), device="cuda")
     raw2 = torch.empty_like(raw)
