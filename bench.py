@@ -341,9 +341,15 @@ def main():
         torch.cuda.synchronize()
         # episode statistics: one NCCL all-reduce per timed window (not per step)
         st = env.stats_tensor(clear=False)
+        ar_ms = None
         if world > 1:
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
             dist.all_reduce(st)
+            a1.record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            ar_ms = a0.elapsed_time(a1)
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     local_s = sum(step_ms) / 1e3
@@ -423,6 +429,7 @@ def main():
         "gpu_launches": args.steps,
         "clocks": clocks,
         "episode_stats": stats,
+        "stats_allreduce_ms": max_over_ranks(ar_ms) if world > 1 else None,
         "engine": {k: env.info[k] for k in ("precision", "block", "grid", "step_kernel_registers",
                                             "device_name", "sm_count")},
     }
