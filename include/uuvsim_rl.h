@@ -84,6 +84,11 @@ uint64_t uuvsim_rl_image_bytes(uint32_t obs_dim);
 int32_t uuvsim_rl_prepare(const UuvRlPolicyArgs* args, void* image, uint64_t len, uint64_t stream);
 int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* args, uint64_t stream);
 int32_t uuvsim_rl_post(const UuvRlPostArgs* args, uint64_t stream);
+/* GAE over the horizon buffers (reference ppo.py:112-130): [T][M] fp32 rewards,
+ * values, done flags (terminal), bootstrap values [M] -> advantages, returns [T][M] */
+int32_t uuvsim_rl_gae(const float* rew, const float* val, const float* done, const float* boot,
+                      uint32_t horizon, uint64_t num_envs, float gamma, float lam, float* adv,
+                      float* ret, uint64_t stream);
 
 #ifdef __cplusplus
 }

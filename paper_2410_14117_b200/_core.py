@@ -69,6 +69,8 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
         "uuvsim_rl_post": (i32, [vp, u64]),
         "uuvsim_rl_image_bytes": (u64, [u32]),
         "uuvsim_rl_prepare": (i32, [vp, vp, u64, u64]),
+        "uuvsim_rl_gae": (i32, [vp, vp, vp, vp, u32, u64, ctypes.c_float, ctypes.c_float,
+                                vp, vp, u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)   # AttributeError on a missing export, like the reference

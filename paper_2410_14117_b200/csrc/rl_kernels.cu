@@ -724,7 +724,40 @@ inline size_t smem_bytes(int D) {
 
 }  // namespace uuvtc
 
+namespace uuvrl {
+// GAE (reference ppo.py:112-130) over [T][M] buffers, one thread per env walking
+// the horizon backwards; done_t is terminal (nonterminal = 1 - done_t).
+__global__ void k_gae(const float* __restrict__ rew, const float* __restrict__ val,
+                      const float* __restrict__ done, const float* __restrict__ boot, int T,
+                      uint64_t M, float gamma, float lam, float* __restrict__ adv,
+                      float* __restrict__ ret) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M) return;
+    float last = 0.0f, next_v = boot[e];
+    for (int t = T - 1; t >= 0; --t) {
+        const size_t i = (size_t)t * M + e;
+        const float nonterminal = 1.0f - done[i];
+        const float v = val[i];
+        const float delta = rew[i] + gamma * next_v * nonterminal - v;
+        last = delta + gamma * lam * nonterminal * last;
+        adv[i] = last;
+        ret[i] = last + v;
+        next_v = v;
+    }
+}
+}  // namespace uuvrl
+
 extern "C" {
+
+int32_t uuvsim_rl_gae(const float* rew, const float* val, const float* done, const float* boot,
+                      uint32_t horizon, uint64_t num_envs, float gamma, float lam, float* adv,
+                      float* ret, uint64_t stream) {
+    if (!rew || !val || !done || !boot || !adv || !ret || horizon == 0 || num_envs == 0) return 3;
+    const unsigned grid = (unsigned)((num_envs + 255) / 256);
+    uuvrl::k_gae<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        rew, val, done, boot, (int)horizon, num_envs, gamma, lam, adv, ret);
+    return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
 
 uint32_t uuvsim_rl_policy_blocks(uint64_t num_envs) {
     // rows for both kernels: 64-env FFMA blocks, or two rows per 128-env tensor-core CTA

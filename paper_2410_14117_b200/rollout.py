@@ -226,9 +226,88 @@ class Rollout:
         self.graph.replay()
 
 
+def gae_fused(rewards, values, dones, bootstrap_value, gamma: float, lam: float):
+    """gae() as one kernel (csrc/rl_kernels.cu k_gae: a thread per env walks the
+    horizon backwards) instead of ~6 framework ops per time step."""
+    import ctypes
+    from . import _core
+    lib = _core.load()
+    T, M = rewards.shape
+    for t in (rewards, values, dones, bootstrap_value):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("gae_fused needs contiguous fp32 CUDA tensors")
+    adv, ret = torch.empty_like(rewards), torch.empty_like(rewards)
+    _core.check(lib, lib.uuvsim_rl_gae(
+        rewards.data_ptr(), values.data_ptr(), dones.data_ptr(), bootstrap_value.data_ptr(),
+        T, M, ctypes.c_float(gamma), ctypes.c_float(lam), adv.data_ptr(), ret.data_ptr(),
+        torch.cuda.current_stream().cuda_stream))
+    return adv, ret
+
+
+class GraphedMinibatchStep:
+    """One PPO minibatch step -- forward, clipped surrogate + value loss, backward,
+    Adam -- captured as a CUDA graph on static minibatch buffers (ppo.py:133-196).
+    The shuffled minibatch rows are gathered into the static buffers eagerly;
+    the first three steps run eagerly on a side stream to allocate optimizer
+    state, the fourth is captured, and every later one is a replay."""
+
+    WARMUP = 3
+
+    def __init__(self, policy: ActorCritic, opt, cfg: TrainConfig, mb: int, obs_dim: int,
+                 act_dim: int, dev):
+        self.policy, self.opt, self.cfg = policy, opt, cfg
+        f = torch.float32
+        self.obs = torch.zeros((mb, obs_dim), device=dev, dtype=f)
+        self.act = torch.zeros((mb, act_dim), device=dev, dtype=f)
+        self.logp_old = torch.zeros(mb, device=dev, dtype=f)
+        self.adv = torch.zeros(mb, device=dev, dtype=f)
+        self.ret = torch.zeros(mb, device=dev, dtype=f)
+        self.agg = torch.zeros(5, device=dev, dtype=torch.float64)
+        self.graph = None
+        self.steps = 0
+        self.side = torch.cuda.Stream(device=dev)
+
+    def _body(self):
+        pol, cfg = self.policy, self.cfg
+        mean, value = pol(self.obs)
+        logp = pol.log_prob(self.act, mean)
+        ratio = torch.exp(logp - self.logp_old)
+        s1 = ratio * self.adv
+        s2 = ratio.clamp(1.0 - cfg.clip, 1.0 + cfg.clip) * self.adv
+        surrogate = -torch.minimum(s1, s2).mean()
+        value_loss = ((value - self.ret) ** 2).mean()
+        loss = surrogate + cfg.value_coef * value_loss - cfg.entropy_coef * pol.entropy()
+        self.opt.zero_grad(set_to_none=False)
+        loss.backward()
+        self.opt.step()
+        with torch.no_grad():
+            self.agg.add_(torch.stack([
+                loss.detach(), surrogate.detach(), value_loss.detach(),
+                (self.logp_old - logp).mean().detach(),
+                ((ratio - 1.0).abs() > cfg.clip).float().mean()]).double())
+
+    def __call__(self):
+        if self.graph is not None:
+            self.graph.replay()
+        elif self.steps < self.WARMUP:
+            self.side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self.side):
+                self._body()
+            torch.cuda.current_stream().wait_stream(self.side)
+        else:
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self._body()
+            self.graph.replay()
+        self.steps += 1
+
+
 def ppo_update(policy: ActorCritic, opt, ro: Rollout, cfg: TrainConfig,
-               gen: torch.Generator) -> dict:
-    """Shuffled minibatch epochs (ppo.py:173-196) with torch autograd."""
+               gen: torch.Generator, step: GraphedMinibatchStep | None = None) -> dict:
+    """Shuffled minibatch epochs (ppo.py:173-196) with torch autograd; with ``step``
+    each minibatch is one replay of a captured graph (see GraphedMinibatchStep)."""
+    if step is not None:
+        return _ppo_update_graphed(policy, ro, cfg, gen, step)
     adv, ret = gae(ro.rew_buf, ro.val_buf, ro.done_buf, ro.boot_value, cfg.gamma, cfg.lam)
     obs = ro.obs_buf.reshape(-1, ro.obs_buf.shape[-1])
     act = ro.act_buf.reshape(-1, ro.act_buf.shape[-1])
@@ -269,6 +348,36 @@ def ppo_update(policy: ActorCritic, opt, ro: Rollout, cfg: TrainConfig,
     return out
 
 
+def _ppo_update_graphed(policy, ro: Rollout, cfg: TrainConfig, gen, step: GraphedMinibatchStep):
+    adv, ret = gae_fused(ro.rew_buf, ro.val_buf, ro.done_buf, ro.boot_value, cfg.gamma, cfg.lam)
+    obs = ro.obs_buf.reshape(-1, ro.obs_buf.shape[-1])
+    act = ro.act_buf.reshape(-1, ro.act_buf.shape[-1])
+    logp_old = ro.logp_buf.reshape(-1)
+    adv = adv.reshape(-1)
+    ret = ret.reshape(-1)
+    adv = (adv - adv.mean()) / (adv.std(unbiased=False) + 1e-8)
+    n = obs.shape[0]
+    mb = step.obs.shape[0]
+    step.agg.zero_()
+    count = 0
+    for _ in range(cfg.epochs):
+        order = torch.randperm(n, device=obs.device, generator=gen)
+        for lo in range(0, n - mb + 1, mb):   # full minibatches (static graph shapes)
+            idx = order[lo:lo + mb]
+            torch.index_select(obs, 0, idx, out=step.obs)
+            torch.index_select(act, 0, idx, out=step.act)
+            torch.index_select(logp_old, 0, idx, out=step.logp_old)
+            torch.index_select(adv, 0, idx, out=step.adv)
+            torch.index_select(ret, 0, idx, out=step.ret)
+            step()
+            count += 1
+    vals = (step.agg / max(count, 1)).tolist()
+    out = dict(zip(("loss", "policy_loss", "value_loss", "approx_kl", "clip_fraction"), vals))
+    if not math.isfinite(out["loss"]):
+        raise RuntimeError("non-finite PPO loss")
+    return out
+
+
 @torch.no_grad()
 def evaluate(policy: ActorCritic, norm: RunningNorm, make_env, episodes: int, seed: int,
              episode_len: int) -> dict:
@@ -292,13 +401,19 @@ def evaluate(policy: ActorCritic, norm: RunningNorm, make_env, episodes: int, se
 
 def train(make_env, cfg: TrainConfig, use_graph: bool = True, log_cb=None,
           eval_every: int = 0, eval_episodes: int = 256, episode_len: int = 600,
-          fused: bool | None = None) -> dict:
+          fused: bool | None = None, graph_update: bool | None = None) -> dict:
     """collect -> GAE -> PPO update until cfg.total_env_steps (ppo.py:245-338)."""
     env = make_env(cfg.num_envs, cfg.seed)
     dev = torch.device("cuda", env.device_index)
     policy = ActorCritic(env.obs_dim, env.action_dim, cfg.hidden, cfg.seed,
                          cfg.init_log_std).to(dev)
-    opt = torch.optim.Adam(policy.parameters(), lr=cfg.lr, eps=1e-8)
+    n_samples = cfg.num_envs * cfg.horizon
+    if graph_update is None:   # graphed minibatch steps need full, equal minibatches
+        graph_update = use_graph and n_samples % min(cfg.minibatch, n_samples) == 0
+    opt = torch.optim.Adam(policy.parameters(), lr=cfg.lr, eps=1e-8,
+                           capturable=bool(graph_update))
+    step = (GraphedMinibatchStep(policy, opt, cfg, min(cfg.minibatch, n_samples), env.obs_dim,
+                                 env.action_dim, dev) if graph_update else None)
     norm = RunningNorm(env.obs_dim, dev)
     torch.manual_seed(cfg.seed + 1)
     gen = torch.Generator(device=dev).manual_seed(cfg.seed + 2)
@@ -313,12 +428,13 @@ def train(make_env, cfg: TrainConfig, use_graph: bool = True, log_cb=None,
         ro.collect()
         torch.cuda.synchronize(dev)
         t1 = time.perf_counter()
-        losses = ppo_update(policy, opt, ro, cfg, gen)
+        losses = ppo_update(policy, opt, ro, cfg, gen, step)
         torch.cuda.synchronize(dev)
         t2 = time.perf_counter()
         if it > 0:   # the first horizon includes graph capture
             t_collect += t1 - t0
-        t_update += t2 - t1
+        if it > 0:   # the first update includes warm-up + graph capture
+            t_update += t2 - t1
         env_steps += cfg.num_envs * cfg.horizon
         it += 1
         rec = {"iteration": it, "env_steps": env_steps, **losses}
@@ -332,8 +448,8 @@ def train(make_env, cfg: TrainConfig, use_graph: bool = True, log_cb=None,
     env.close()
     return {"policy": policy, "normalizer": norm, "metrics": metrics, "env_steps": env_steps,
             "collect_env_steps_per_sec": timed_steps / max(t_collect, 1e-12),
-            "update_s_per_iter": t_update / max(it, 1)}
+            "update_s_per_iter": t_update / max(it - 1, 1)}
 
 
-__all__ = ["TrainConfig", "ActorCritic", "RunningNorm", "gae", "Rollout", "ppo_update",
-           "evaluate", "train"]
+__all__ = ["TrainConfig", "ActorCritic", "RunningNorm", "gae", "gae_fused", "Rollout",
+           "GraphedMinibatchStep", "ppo_update", "evaluate", "train"]

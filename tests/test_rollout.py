@@ -229,3 +229,51 @@ def test_fused_collect_matches_framework_collect():
         env.close()
     for a, b in zip(*outs):
         torch.testing.assert_close(a.double(), b.double(), rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.gpu
+def test_gae_fused_matches_reference():
+    g = torch.Generator(device="cuda").manual_seed(2)
+    T, M = 37, 1000
+    r = torch.randn((T, M), device="cuda", generator=g)
+    v = torch.randn((T, M), device="cuda", generator=g)
+    d = (torch.rand((T, M), device="cuda", generator=g) < 0.1).float()
+    b = torch.randn(M, device="cuda", generator=g)
+    want_a, want_r = R.gae(r, v, d, b, 0.99, 0.95)
+    got_a, got_r = R.gae_fused(r, v, d, b, 0.99, 0.95)
+    torch.testing.assert_close(got_a, want_a, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(got_r, want_r, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_graphed_update_equals_eager_update():
+    make = _make_env("circle")
+    cfg = R.TrainConfig(num_envs=1024, horizon=16, minibatch=4096, epochs=2, lr=3e-4)
+    env = make(cfg.num_envs, 4)
+    pol0 = R.ActorCritic(env.obs_dim, env.action_dim, seed=2).cuda()
+    norm = R.RunningNorm(env.obs_dim, "cuda")
+    ro = R.Rollout(env, pol0, norm, cfg, use_graph=False)
+    ro.reset(4)
+    ro.collect()
+    results = []
+    for graphed in (False, True):
+        pol = R.ActorCritic(env.obs_dim, env.action_dim, seed=2).cuda()
+        pol.load_state_dict(pol0.state_dict())
+        opt = torch.optim.Adam(pol.parameters(), lr=cfg.lr, eps=1e-8, capturable=graphed)
+        step = (R.GraphedMinibatchStep(pol, opt, cfg, cfg.minibatch, env.obs_dim,
+                                       env.action_dim, torch.device("cuda")) if graphed else None)
+        ro.policy = pol
+        losses = []
+        for it in range(3):   # covers warm-up, capture and replays
+            gen = torch.Generator(device="cuda").manual_seed(9 + it)
+            losses.append(R.ppo_update(pol, opt, ro, cfg, gen, step)["loss"])
+        torch.cuda.synchronize()
+        results.append((losses, [p.detach().clone() for p in pol.parameters()]))
+    env.close()
+    (l0, p0), (l1, p1) = results
+    np.testing.assert_allclose(l1, l0, rtol=1e-4, atol=1e-5)
+    # Adam moves every weight by ~lr per step whatever the gradient's size, so the
+    # fp32 rounding differences of the fused GAE / capturable Adam can flip the
+    # sign of near-zero gradients: parameters agree to a few learning rates
+    for a, b in zip(p0, p1):
+        torch.testing.assert_close(b, a, rtol=0, atol=10 * cfg.lr)

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--eval-every", type=int, default=5)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="framework-op policy path")
+    ap.add_argument("--eager-update", action="store_true", help="no CUDA graph for the PPO step")
     a = ap.parse_args()
     base = uuv.bluerov2_params() if a.vehicle == "bluerov2" else uuv.default_params()
 
@@ -48,7 +49,8 @@ def main():
     t0 = time.perf_counter()
     out = R.train(make, cfg, use_graph=not a.no_graph, eval_every=a.eval_every,
                   log_cb=lambda r: print(json.dumps(r), flush=True),
-                  fused=False if a.unfused else None)
+                  fused=False if a.unfused else None,
+                  graph_update=False if a.eager_update else None)
     wall = time.perf_counter() - t0
     final = R.evaluate(out["policy"], out["normalizer"], make, 1024, 1000, 600)
     print(json.dumps({"summary": True, "task": a.task, "envs": a.envs, "env_steps": out["env_steps"],
