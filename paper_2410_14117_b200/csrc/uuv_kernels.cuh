@@ -71,6 +71,10 @@ struct StatAcc {
 // the LA_PRE+1 trajectory rows the reward and observation will need).
 constexpr int LA_PRE = 5;
 
+#ifndef UUV_EPI_UNROLL
+#define UUV_EPI_UNROLL 1
+#endif
+
 // RR: the LA_PRE+1 trajectory rows ride in registers across the sub-steps.
 // Where registers are short (randomised or paired kernels) ptxas would park
 // them in local memory -- an STL that waits for the loads before the first
@@ -135,6 +139,20 @@ __device__ __forceinline__ void write_obs(const TaskP<T>& tk, O* __restrict__ ro
                     q[1] = V2<O>{(O)(r.z - s[2]), ephi};
                     q[2] = V2<O>{eth, (O)obs_wrap<T>(r.w - s[5])};
                 }
+            }
+        } else if (UUV_EPI_UNROLL && tk.lookahead <= LA_PRE) {
+            // table rows (L1 hits after load_env's prefetch): issue all loads first
+            V4<T> r[LA_PRE];
+#pragma unroll
+            for (int k = 1; k <= LA_PRE; ++k)
+                r[k - 1] = k <= tk.lookahead ? tk.traj[min(nstep + k, tab_last)] : V4<T>{};
+#pragma unroll
+            for (int k = 1; k <= LA_PRE; ++k) {
+                if (k > tk.lookahead) break;
+                V2<O>* q = o2 + 3 * (k - 1);
+                q[0] = V2<O>{(O)(r[k - 1].x - s[0]), (O)(r[k - 1].y - s[1])};
+                q[1] = V2<O>{(O)(r[k - 1].z - s[2]), ephi};
+                q[2] = V2<O>{eth, (O)obs_wrap<T>(r[k - 1].w - s[5])};
             }
         } else {
 #pragma unroll 1
