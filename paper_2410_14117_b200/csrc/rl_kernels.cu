@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 
@@ -296,13 +297,21 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
     if (threadIdx.x == 0 && a.noise_ctr) *a.noise_ctr += 1;
 }
 
+// dynamic shared memory opt-in, once per kernel and device (attributes are per
+// device context)
+template <auto KERNEL> static void smem_optin(int bytes) {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+}
+
 template <int DP> static cudaError_t launch_policy(const UuvRlPolicyArgs& a, cudaStream_t st) {
     const size_t smem = (size_t)Lay<DP>::total * sizeof(float);
-    static bool once = (cudaFuncSetAttribute(k_policy_act<DP>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        true);
-    (void)once;
+    smem_optin<k_policy_act<DP>>((int)smem);
     const unsigned grid = (unsigned)((a.num_envs + ENVS - 1) / ENVS);
     k_policy_act<DP><<<grid, BLK, smem, st>>>(a);
     return cudaGetLastError();
@@ -787,12 +796,7 @@ int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* a, uint64_t stream) {
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (a->wimage) {   // tensor cores
         const size_t smem = uuvtc::smem_bytes((int)a->obs_dim);
-        static int max_set = 0;
-        if ((int)smem > max_set) {
-            cudaFuncSetAttribute(uuvtc::k_policy_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)uuvtc::smem_bytes(36));
-            max_set = (int)uuvtc::smem_bytes(36);
-        }
+        uuvrl::smem_optin<uuvtc::k_policy_tc>((int)uuvtc::smem_bytes(36));
         const unsigned grid = (unsigned)((a->num_envs + uuvtc::M - 1) / uuvtc::M);
         uuvtc::k_policy_tc<<<grid, uuvtc::NT, smem, st>>>(*a);
         return cudaGetLastError() == cudaSuccess ? 0 : 4;

@@ -14,6 +14,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <type_traits>
 
@@ -746,10 +748,18 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
 }
 
 // ------------------------------------------------------------------ launchers
-template <class K>
-static void allow_smem(K kernel) {
-    // opt-in above 48 KB once per kernel variant (paired rows in f64: 73.7 KB)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_STAGE_BYTES);
+// opt-in above 48 KB (paired rows in f64: 73.7 KB) once per kernel variant and
+// device: function attributes are per device context, and one process may drive
+// engines on several GPUs
+template <auto KERNEL>
+static void allow_smem() {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_STAGE_BYTES);
+    done.fetch_or(bit, std::memory_order_release);
 }
 
 template <class T>
@@ -765,8 +775,7 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
             const size_t smem = (size_t)2 * (3 * 2 * BLOCK * 16 + (UUV_TMA_ACT ? 2 * BLOCK * p.act_dim * 4 : 0));
 #define UUV_T(M)                                                                        \
     do {                                                                                \
-        static bool once = (allow_smem(k_step_pair_tma<M>), true);                      \
-        (void)once;                                                                     \
+        allow_smem<k_step_pair_tma<M>>();                                               \
         k_step_pair_tma<M><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason);  \
     } while (0)
             if (mix) UUV_T(true); else UUV_T(false);
@@ -778,8 +787,7 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
             const size_t smem = p.stage_obs ? (size_t)2 * BLOCK * p.task.obs_dim * esz : 0;
 #define UUV_P(TR, M)                                                                   \
     do {                                                                               \
-        static bool once = (allow_smem(k_step_pair<TR, M>), true);                     \
-        (void)once;                                                                    \
+        allow_smem<k_step_pair<TR, M>>();                                              \
         k_step_pair<TR, M><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
     } while (0)
             if (track) { if (mix) UUV_P(true, true); else UUV_P(true, false); }
@@ -792,8 +800,7 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
     const size_t smem = p.stage_obs ? (size_t)BLOCK * p.task.obs_dim * esz : 0;
 #define UUV_L(TR, D, M, PAT)                                                                 \
     do {                                                                                     \
-        static bool once = (allow_smem(k_step<T, TR, D, M, PAT>), true);                     \
-        (void)once;                                                                          \
+        allow_smem<k_step<T, TR, D, M, PAT>>();                                              \
         k_step<T, TR, D, M, PAT><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
     } while (0)
 #define UUV_LP(TR, D, M) \
