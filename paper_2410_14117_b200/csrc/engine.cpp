@@ -1007,8 +1007,19 @@ void Engine::stats_host(double* out, bool clear) {
 }
 
 // ------------------------------------------------------------------ device face
+// device-face calls launch on the caller's stream without switching devices (that
+// would change the caller's current device): refuse loudly when it is not ours
+void Engine::check_device() const {
+    int cur = -1;
+    cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != device_)
+        throw RuntimeError("device face called with current CUDA device " + std::to_string(cur) +
+                           "; this engine lives on device " + std::to_string(device_));
+}
+
 void Engine::dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8_t* reason,
                       cudaStream_t st) {
+    check_device();
     const bool track = task_.kind != 0, dr = ranges_.enabled;
     if (fp64_)
         cuda_check(Launch<double>::step(*pd_, track, dr, fossen_, pair_, (const double*)act,
@@ -1019,6 +1030,7 @@ void Engine::dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8
 }
 
 void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
+    check_device();
     if (fp64_) {
         pd_->seed = seed;
         cuda_check(Launch<double>::reset(*pd_, (double*)obs, st), "dev_reset");
@@ -1029,6 +1041,7 @@ void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
 }
 
 void Engine::dev_observe(void* obs, cudaStream_t st) {
+    check_device();
     if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
 }
@@ -1039,11 +1052,13 @@ void Engine::dev_set_final_obs(void* buf) {
 }
 
 void Engine::dev_states(void* out, cudaStream_t st) {
+    check_device();
     if (fp64_) cuda_check(Launch<double>::pack_states_t(*pd_, (double*)out, st), "dev_states");
     else cuda_check(Launch<float>::pack_states_t(*pf_, (float*)out, st), "dev_states");
 }
 
 void Engine::dev_bench_actions(void* act, cudaStream_t st) {
+    check_device();
     const uint64_t seed = fp64_ ? pd_->seed : pf_->seed;
     cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_,
                                     fp64_ ? nullptr : (float*)act,
@@ -1051,6 +1066,7 @@ void Engine::dev_bench_actions(void* act, cudaStream_t st) {
 }
 
 void Engine::dev_stats(double* out, bool clear, cudaStream_t st) {
+    check_device();
     cuda_check(launch_stats_reduce(stats_part_, nblk_, out, clear ? 1 : 0, st), "dev_stats");
 }
 
@@ -1078,6 +1094,7 @@ void Engine::graph_capture(const void* act, void* obs, void* rew, uint8_t* done,
 }
 
 void Engine::graph_launch(cudaStream_t st) {
+    check_device();
     if (!graph_exec_) throw RuntimeError("no captured graph (call uuvsim_dev_graph_capture first)");
     cuda_check(cudaGraphLaunch(graph_exec_, st), "GraphLaunch");
 }

@@ -106,6 +106,7 @@ public:
     void synchronize();
     std::string info() const;
     void activate() const;
+    void check_device() const;
 
 private:
     void parse(const std::string& text);
