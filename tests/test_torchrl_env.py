@@ -98,3 +98,63 @@ def test_final_obs_not_written_by_host_abi_step():
     torch.cuda.synchronize()
     assert torch.all(vec.final_obs == 7.0)
     vec.close()
+
+
+def _fake_torchrl(monkeypatch):
+    """Minimal stand-ins for tensordict / torchrl (not installed in this image) so the
+    import-gated EnvBase subclass can be exercised."""
+    import sys
+    import types
+
+    class TensorDict(dict):
+        def __init__(self, d, batch_size=None, device=None):
+            super().__init__(d)
+            self.batch_size, self.device = batch_size, device
+
+        def get(self, k, default=None):
+            return dict.get(self, k, default)
+
+    class EnvBase:
+        def __init__(self, device=None, batch_size=None):
+            self.device, self.batch_size = device, batch_size
+
+    class Spec:
+        def __init__(self, *a, **kw):
+            self.args, self.kw = a, kw
+
+    td = types.ModuleType("tensordict")
+    td.TensorDict = TensorDict
+    trl = types.ModuleType("torchrl")
+    envs = types.ModuleType("torchrl.envs")
+    envs.EnvBase = EnvBase
+    data = types.ModuleType("torchrl.data")
+    for name in ("Composite", "Unbounded", "Bounded", "Categorical"):
+        setattr(data, name, type(name, (Spec,), {}))
+    trl.envs, trl.data = envs, data
+    for k, v in (("tensordict", td), ("torchrl", trl), ("torchrl.envs", envs),
+                 ("torchrl.data", data)):
+        monkeypatch.setitem(sys.modules, k, v)
+    return TensorDict
+
+
+@pytest.mark.gpu
+def test_torchrl_env_protocol_with_stand_in_modules(monkeypatch):
+    TensorDict = _fake_torchrl(monkeypatch)
+    L, n = 6, 512
+    vec = T.VecEnv(uuv.B200EnvBatch(_cfg("circle", L, n, False), 3))
+    env = T.make_torchrl_env(vec, seed=3)
+    assert tuple(env.batch_size) == (n,)
+    td0 = env._reset(None)
+    assert td0["observation"].shape == (n, vec.obs_dim) and not td0["done"].any()
+    act = torch.zeros((n, vec.action_dim), device=vec.device)
+    for t in range(L):
+        td = env._step(TensorDict({"action": act}))
+        assert td["reward"].shape == (n, 1) and td["done"].shape == (n, 1)
+        assert torch.equal(td["done"], td["terminated"] | td["truncated"])
+    assert td["truncated"].all()                       # every env hits episode_len
+    # the terminal observation is reported; the collector's partial reset gets the
+    # already reset observation from the engine
+    post = env._reset(TensorDict({"_reset": td["done"].clone()}))["observation"]
+    assert not torch.equal(post, td["observation"])
+    assert torch.equal(post, vec.batch.observe_tensors())
+    vec.close()
