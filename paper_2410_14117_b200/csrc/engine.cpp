@@ -1128,6 +1128,8 @@ std::string Engine::info() const {
         {"tma_pipelined", (fp64_ ? 0 : pf_->persist_blocks) > 0},
         {"stage_obs", (fp64_ ? pd_->stage_obs : pf_->stage_obs) != 0},
         {"host_io", host_io_ == 0 ? "copy" : host_io_ == 1 ? "mapped" : "auto"},
+        {"arena_address", (uint64_t)(uintptr_t)arena_},
+        {"arena_bytes", (uint64_t)arena_used_},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},

@@ -1,0 +1,50 @@
+"""C3 ablation: per-step device time (L2 flushed) with features toggled.
+
+    python tools/c3_ablation.py
+"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import paper_2410_14117_b200 as uuv  # noqa: E402
+
+
+def timed(cfg, steps=300):
+    env = uuv.B200EnvBatch(cfg, 0, pinned=False)
+    act = env.bench_actions_tensor()
+    env.capture_graph(act, 1)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    for _ in range(10):
+        env.replay_graph()
+    evs = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        env.replay_graph()
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    env.close()
+    ts = sorted(x.elapsed_time(y) * 1e3 for x, y in evs)
+    return round(ts[len(ts) // 2], 2)
+
+
+def main():
+    heavy = uuv.default_params()
+    cases = [("lemniscate", True, True, 5), ("lemniscate", False, True, 5),
+             ("lemniscate", True, False, 5), ("station_keeping", True, True, 5),
+             ("lemniscate", True, True, 1)]
+    for kind, dr, stats, la in cases + cases[::-1]:
+        spec = uuv.TaskSpec(kind=kind, lookahead=la)
+        ranges = uuv.default_ranges(per_episode=True) if dr else None
+        cfg = uuv.engine_config_dict(heavy, spec, 65536, 0, 0, ranges, device=0, stats=stats)
+        print(json.dumps({"kind": kind, "dr": dr, "stats": stats, "lookahead": la,
+                          "median_us": timed(cfg)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
