@@ -40,8 +40,10 @@ extern "C" {
 uint32_t uuvsim_abi_version(void);
 
 /* capi.rs:79-98 -- create an engine from a UTF-8 JSON config (engine.rs:17-94
- * schema; extra keys: "vehicles", batch.vehicle_mix, batch.env_offset,
- * "device": {"precision": "fp32"|"fp64", "index": n, "stats": bool}) */
+ * schema; extra keys, ignored by the reference's parser: "vehicles",
+ * batch.vehicle_mix, batch.env_offset, "device": {"precision": "fp32"|"fp64",
+ * "index": n, "stats": bool, "host_io": "auto"|"copy"|"mapped",
+ * "pair"/"stage_obs": "auto"|"on"|"off", "pattern": "auto"|"dense", "tma": bool}) */
 int32_t uuvsim_create(const char* config_json, uint64_t* out_handle);
 
 /* capi.rs:102-120 -- out[4] = {num_envs, obs_dim, action_dim, episode_len} */
