@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import paper_2410_14117_b200 as uuv  # noqa: E402
 
 
-def timed(cfg, steps=300):
+def timed(cfg, steps=300, read_flush=False):
     env = uuv.B200EnvBatch(cfg, 0, pinned=False)
     act = env.bench_actions_tensor()
     env.capture_graph(act, 1)
@@ -20,8 +20,12 @@ def timed(cfg, steps=300):
     for _ in range(10):
         env.replay_graph()
     evs = []
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
     for _ in range(steps):
-        flush.zero_()
+        if read_flush:   # evict with reads: the L2 ends clean instead of dirty
+            torch.sum(flush, dim=0, out=sink)
+        else:
+            flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         env.replay_graph()
@@ -35,6 +39,14 @@ def timed(cfg, steps=300):
 
 def main():
     heavy = uuv.default_params()
+    spec = uuv.TaskSpec(kind="lemniscate")
+    cfg = uuv.engine_config_dict(heavy, spec, 65536, 0, 0, uuv.default_ranges(per_episode=True),
+                                 device=0)
+    for rf in (False, True, False, True):
+        print(json.dumps({"c3": True, "read_flush": rf, "median_us": timed(cfg, read_flush=rf)}),
+              flush=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "flush-only":
+        return
     cases = [("lemniscate", True, True, 5), ("lemniscate", False, True, 5),
              ("lemniscate", True, False, 5), ("station_keeping", True, True, 5),
              ("lemniscate", True, True, 1)]
