@@ -57,3 +57,17 @@ def test_gpu_arm_line():
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"]
     assert d["gpu_launches"] == 20
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """Driver launch for N > 1: rank 0 alone runs and prints; the others exit 0."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29531", str(ROOT / "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2

@@ -42,8 +42,11 @@ def main():
     spec = uuv.TaskSpec(kind="lemniscate")
     cfg = uuv.engine_config_dict(heavy, spec, 65536, 0, 0, uuv.default_ranges(per_episode=True),
                                  device=0)
+    c2 = uuv.engine_config_dict(uuv.bluerov2_params(), uuv.TaskSpec(), 4096, 0, 0, None, device=0)
     for rf in (False, True, False, True):
         print(json.dumps({"c3": True, "read_flush": rf, "median_us": timed(cfg, read_flush=rf)}),
+              flush=True)
+        print(json.dumps({"c2": True, "read_flush": rf, "median_us": timed(c2, read_flush=rf)}),
               flush=True)
     if len(sys.argv) > 1 and sys.argv[1] == "flush-only":
         return
