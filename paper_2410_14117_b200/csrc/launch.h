@@ -19,12 +19,21 @@ constexpr int BLOCK = UUV_BLOCK;   // threads per block of the env kernels (one 
 #ifndef UUV_STEP_MIN_BLOCKS_DR
 #define UUV_STEP_MIN_BLOCKS_DR 6   // with per-env randomised M/L in registers: 85
 #endif
+#ifndef UUV_STEP_MIN_BLOCKS_TRACK
+#define UUV_STEP_MIN_BLOCKS_TRACK 6   // tracking (lookahead rows in registers): 85, no spills
+#endif
+#ifndef UUV_STEP_MIN_BLOCKS_F64
+#define UUV_STEP_MIN_BLOCKS_F64 4     // fp64 parity mode: 128 (doubles take register pairs;
+                                      // measured: C3 fp64 73.5 -> 45.5 us, C5 371 -> 400 us)
+#endif
 #ifndef UUV_PAIR_MIN_BLOCKS
 #define UUV_PAIR_MIN_BLOCKS 6      // two envs per thread: 85
 #endif
 constexpr int STEP_MIN_BLOCKS = UUV_STEP_MIN_BLOCKS;
 constexpr int STEP_MIN_BLOCKS_DR = UUV_STEP_MIN_BLOCKS_DR;
 constexpr int PAIR_MIN_BLOCKS = UUV_PAIR_MIN_BLOCKS;
+constexpr int STEP_MIN_BLOCKS_TRACK = UUV_STEP_MIN_BLOCKS_TRACK;
+constexpr int STEP_MIN_BLOCKS_F64 = UUV_STEP_MIN_BLOCKS_F64;
 
 #ifndef UUV_PAIR_AUTO_MIN_ENVS
 #define UUV_PAIR_AUTO_MIN_ENVS 131072

@@ -10,7 +10,8 @@ flt = sys.argv[1] if len(sys.argv) > 1 else ""
 cur = None
 rows = {}
 for line in sys.stdin:
-    m = re.search(r"(?:Compiling entry function|Function properties for) '([^']+)'", line)
+    m = (re.search(r"Compiling entry function '([^']+)'", line) or
+         re.search(r"Function properties for '?([A-Za-z0-9_$.]+)'?", line))
     if m:
         cur = m.group(1)
         rows.setdefault(cur, {})
