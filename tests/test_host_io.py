@@ -122,3 +122,16 @@ def test_raw_abi_with_alternating_pinned_buffers():
         del bufs, arrs
     env.close()
     ref.close()
+
+
+def test_bench_throughput_and_bench_actions_match_reference_protocol():
+    env = uuv.batch_create(uuv.TaskSpec(), uuv.bluerov2_params(), None, 1024, 7, device=0)
+    host = uuv.bench_actions(env)                   # reference batch.py:168-176 (f64 host)
+    dev = env.bench_actions_tensor().double().cpu().numpy()
+    assert np.array_equal(dev, host.astype(np.float32).astype(np.float64))
+    r = uuv.bench_throughput(env, 20, threads=4)    # reference batch.py:179-197
+    assert set(r) == {"env_steps_per_sec", "wall_time_s", "n_steps", "num_envs", "threads",
+                      "backend"}
+    assert r["n_steps"] == 20 and r["num_envs"] == 1024 and r["threads"] == 4
+    assert r["backend"] == "b200" and r["env_steps_per_sec"] > 0
+    env.close()
