@@ -28,7 +28,7 @@ from tests.test_gpu_parity import CONFIGS, _cfg  # noqa: E402
 
 def teacher_forced(cfg, steps=36):
     gpu = uuv.B200EnvBatch(cfg)
-    ref = orc.OracleBatch(cfg, threads=8)
+    ref = orc.OracleBatch(cfg, threads=0)
     act = orc.bench_actions(cfg["seed"], ref.num_envs, ref.action_dim)
     worst = np.zeros(12)
     worst_scaled = np.zeros(12)
@@ -66,7 +66,7 @@ def teacher_forced(cfg, steps=36):
 
 def rollout(cfg, steps=100, scale=0.3):
     gpu = uuv.B200EnvBatch(cfg)
-    ref = orc.OracleBatch(cfg, threads=8)
+    ref = orc.OracleBatch(cfg, threads=0)
     act = scale * orc.bench_actions(cfg["seed"], ref.num_envs, ref.action_dim)
     ever = np.zeros(ref.num_envs, dtype=bool)
     drift = []
@@ -88,11 +88,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/parity.json")
     ap.add_argument("--configs", default=",".join(CONFIGS))
+    ap.add_argument("--envs", type=int, default=0, help="override num_envs of every config")
+    ap.add_argument("--tf-steps", type=int, default=36)
+    ap.add_argument("--md", default="", help="also write a markdown summary here")
     args = ap.parse_args()
     rep = {}
     for name in args.configs.split(","):
-        cfg = _cfg(**CONFIGS[name])
-        rep[name] = {"teacher_forced": teacher_forced(cfg), "rollout_0.3": rollout(cfg)}
+        kw = dict(CONFIGS[name])
+        if args.envs:
+            kw["n"] = args.envs
+        cfg = _cfg(**kw)
+        rep[name] = {"num_envs": cfg["batch"]["num_envs"],
+                     "teacher_forced": teacher_forced(cfg, args.tf_steps),
+                     "rollout_0.3": rollout(cfg)}
         tf = rep[name]["teacher_forced"]
         print(name, "tf max_err/tol", np.round(tf["max_err_over_tol"], 3).tolist(),
               "outside", tf["n_outside"], "rollout drift", rep[name]["rollout_0.3"]["max_drift"],
@@ -104,6 +112,31 @@ def main():
               rep[prec_name]["rollout_1.0"]["max_drift"], flush=True)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(rep, indent=1))
+    if args.md:
+        names = ("x", "y", "z", "phi", "theta", "psi", "u", "v", "w", "p", "q", "r")
+        lines = ["# Parity report (B200 fp32 engine vs the C oracle)", "",
+                 "Teacher-forced single steps from the oracle state (every env, every step),",
+                 "tolerance 1e-6 + 1e-5|b| per component (angles mod 2 pi), pitch band |theta| > 1.4",
+                 "excluded as the contract states; free rollouts at 0.3 x bench actions.", "",
+                 "| config | envs | env-steps | worst err / tol (component) | outside tol | done mismatch | band env-steps | 100-step drift |",
+                 "|---|---|---|---|---|---|---|---|"]
+        for name, r in rep.items():
+            if "teacher_forced" not in r:
+                continue
+            tf, ro = r["teacher_forced"], r["rollout_0.3"]
+            w = int(np.argmax(tf["max_err_over_tol"]))
+            lines.append(f"| {name} | {r['num_envs']} | {tf['env_steps']} | "
+                         f"{max(tf['max_err_over_tol']):.3f} ({names[w]}) | {tf['n_outside']} | "
+                         f"{tf['done_mismatch'] + ro['done_mismatch']} | {tf['n_band_env_steps']} | "
+                         f"{ro['max_drift']:.2e} |")
+        for name, r in rep.items():
+            if "teacher_forced" in r:
+                continue
+            lines.append("")
+            lines.append(f"{name}: fp64 engine, 150-step rollouts: max drift "
+                         f"{r['rollout_0.3']['max_drift']:.2e} (0.3 x bench actions), "
+                         f"{r['rollout_1.0']['max_drift']:.2e} (full bench actions)")
+        Path(args.md).write_text("\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
