@@ -140,3 +140,39 @@ def test_tiny_and_ragged_batches(n):
     assert np.array_equal(g.step_counts(), o.step_counts())
     g.close()
     o.close()
+
+
+def test_slab_beyond_device_memory_is_a_config_error():
+    import ctypes
+    import json
+    cfg = _cfg(n=1 << 30)                       # ~300 GB with staging: cannot fit
+    lib = uuv._core.load()
+    h = ctypes.c_uint64(0)
+    code = lib.uuvsim_create(json.dumps(cfg).encode(), ctypes.byref(h))
+    assert code == 1
+    assert "MiB of device memory" in uuv._core.last_error(lib)
+
+
+@pytest.mark.slow
+def test_maximum_slab_high_indices_exact():
+    """2^27 envs (~45 GB with the ABI staging): the last envs of the slab reset
+    exactly like the oracle's envs at the same global index, and a step touches
+    every env (64-bit row offsets everywhere)."""
+    n = 1 << 27
+    cfg = _cfg(n=n, kind="circle")
+    g = uuv.B200EnvBatch(cfg, 9, pinned=False)
+    tail = dict(cfg)
+    tail["batch"] = dict(cfg["batch"], num_envs=64, env_offset=n - 64)
+    o = orc.OracleBatch(tail, threads=0)
+    o.reset_all(9)
+    s = g.states_tensor()
+    torch.cuda.synchronize()
+    assert np.array_equal(s[-64:].double().cpu().numpy(), _fp32(o.states()))
+    act = g.bench_actions_tensor()
+    for _ in range(2):
+        g.step_tensors(act)
+    torch.cuda.synchronize()
+    assert g.stats()["env_steps"] == 2 * n
+    assert int(g.step_counts()[-1]) == 2
+    o.close()
+    g.close()
