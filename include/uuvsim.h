@@ -119,6 +119,20 @@ int32_t uuvsim_restore(uint64_t handle, const void* buf, uint64_t len);
  * env's TERMINAL observation (pre-reset state, terminating step) into its row;
  * other rows are left untouched.  Not used by the host-buffer uuvsim_step. */
 int32_t uuvsim_dev_set_final_obs(uint64_t handle, void* buf, uint64_t len);
+/* PD baseline (reference baseline.py:38-75) over the engine's own state slab:
+ * err_body = R^T (ref_xyz - p), err_ang = (ref_ang - ang + pi) mod 2 pi - pi,
+ * wrench = kp * err - kd * nu, f = pinv(A) wrench, throttle = f / kmax (linear) or
+ * copysign(sqrt(|f| / kmax), f) (quadratic_signed), clamped to [-1, 1].  One
+ * kernel; ref6 is a device pointer to the reference pose (engine precision),
+ * actions [M][action_dim] (engine precision) on the caller's stream. */
+typedef struct {
+    double kp[6], kd[6];
+    double pinv[2][8][6];      /* per vehicle slot: pinv of the 6 x N allocation, [thruster][dof] */
+    double kmax[2][8];
+    int32_t quadratic[2][8];   /* 1 = quadratic_signed, 0 = linear */
+} UuvPdGains;
+int32_t uuvsim_dev_pd_actions(uint64_t handle, const UuvPdGains* gains, const void* ref6,
+                              void* actions, uint64_t actions_len, uint64_t stream);
 /* raw states [M][12] into a device buffer (engine precision) */
 int32_t uuvsim_dev_states(uint64_t handle, void* out, uint64_t len, uint64_t stream);
 int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,

@@ -22,6 +22,7 @@ single-state numpy signature for drop-in use.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -148,6 +149,13 @@ def trajectory_table(spec: TaskSpec, steps: int, dtype=torch.float64, device="cp
     return tab.to(dtype=dtype, device=device)
 
 
+class UuvPdGains(ctypes.Structure):
+    """include/uuvsim.h UuvPdGains (per vehicle slot: pinv [8][6], kmax [8], curve)."""
+    _fields_ = [("kp", ctypes.c_double * 6), ("kd", ctypes.c_double * 6),
+                ("pinv", ((ctypes.c_double * 6) * 8) * 2), ("kmax", (ctypes.c_double * 8) * 2),
+                ("quadratic", (ctypes.c_int32 * 8) * 2)]
+
+
 @dataclass
 class PDActor:
     """evaluate()-compatible PD controller tracking the task reference
@@ -162,6 +170,22 @@ class PDActor:
         self._pinv = np.linalg.pinv(allocation_matrix(self.params))
         self._kmax, self._quad = thruster_table(self.params)
         self._cache = {}
+
+    def engine_gains(self, params2=None) -> UuvPdGains:
+        """Gains + allocation pseudo-inverse for the fused engine kernel; ``params2``
+        gives the second vehicle of a mixed batch (default: the same vehicle)."""
+        g = UuvPdGains()
+        for j in range(6):
+            g.kp[j], g.kd[j] = self.gains.kp[j], self.gains.kd[j]
+        for slot, prm in enumerate((self.params, params2 if params2 is not None else self.params)):
+            pinv = np.linalg.pinv(allocation_matrix(prm))
+            kmax, quad = thruster_table(prm)
+            for i in range(pinv.shape[0]):
+                for j in range(6):
+                    g.pinv[slot][i][j] = float(pinv[i, j])
+                g.kmax[slot][i] = float(kmax[i])
+                g.quadratic[slot][i] = int(bool(quad[i]))
+        return g
 
     def reference(self, step: int) -> np.ndarray:
         return trajectory_table(self.spec, 1, start=int(step))[0].numpy()
@@ -209,9 +233,15 @@ def evaluate_pd(env, actor: PDActor, seed: int, steps: int | None = None,
     errs = torch.empty((steps, m), dtype=dt, device=dev)
     dones = torch.empty((steps, m), dtype=torch.uint8, device=dev)
 
+    fused = hasattr(env, "pd_actions_tensor")
+    gains = actor.engine_gains() if fused else None
+
     def body(t):
-        env.states_tensor(out=states)
-        actor.act(states, table[t], out=act)
+        if fused:   # one kernel over the engine's state slab (uuvsim_dev_pd_actions)
+            env.pd_actions_tensor(gains, table[t], out=act)
+        else:
+            env.states_tensor(out=states)
+            actor.act(states, table[t], out=act)
         _o, r, d, _ = env.step_tensors(act)
         errs[t].copy_(r.neg())
         dones[t].copy_(d)
@@ -250,5 +280,5 @@ def evaluate_pd(env, actor: PDActor, seed: int, steps: int | None = None,
             "dones": dones.cpu().numpy(), "device_ms": ev0.elapsed_time(ev1)}
 
 
-__all__ = ["PDGains", "PDActor", "pd_baseline", "pd_batch", "allocation_matrix",
+__all__ = ["PDGains", "PDActor", "UuvPdGains", "pd_baseline", "pd_batch", "allocation_matrix",
            "thruster_table", "trajectory_table", "evaluate_pd"]

@@ -312,6 +312,20 @@ class B200EnvBatch:
         _core.check(self._lib, self._lib.uuvsim_restore(self._handle, blob, len(blob)))
         self.root_seed = int.from_bytes(blob[32:40], "little")   # SnapHeader.root_seed
 
+    def pd_actions_tensor(self, gains, reference, out=None, stream=None):
+        """PD-baseline throttles [M, action_dim] for the current states, one kernel
+        (uuvsim_dev_pd_actions); ``gains`` from ``baseline.PDActor.engine_gains()``,
+        ``reference`` a device tensor of 6 (engine precision)."""
+        import ctypes
+        import torch
+        if out is None:
+            out = torch.empty((self.num_envs, self.action_dim), dtype=self.dtype,
+                              device=torch.device("cuda", self.device_index))
+        _core.check(self._lib, self._lib.uuvsim_dev_pd_actions(
+            self._handle, ctypes.byref(gains), reference.data_ptr(), out.data_ptr(), out.numel(),
+            self._stream(stream)))
+        return out
+
     def states_tensor(self, out=None, stream=None):
         """Raw states [M, 12] on the device (engine precision), e.g. for PD control."""
         import torch

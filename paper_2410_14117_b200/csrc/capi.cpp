@@ -282,6 +282,17 @@ int32_t uuvsim_dev_bench_actions(uint64_t h, void* act, uint64_t len, uint64_t s
     });
 }
 
+int32_t uuvsim_dev_pd_actions(uint64_t h, const UuvPdGains* g, const void* ref6, void* act,
+                              uint64_t len, uint64_t stream) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t want = (uint64_t)e.num_envs() * e.action_dim();
+        if (!g || !ref6 || !act || len != want)
+            return bad_size("actions", want, e.is_fp64() ? "f64" : "f32");
+        e.dev_pd_actions(*g, ref6, act, as_stream(stream));
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_states(uint64_t h, void* out, uint64_t len, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * 12;

@@ -1051,6 +1051,16 @@ void Engine::dev_set_final_obs(void* buf) {
     else pf_->final_obs = buf;
 }
 
+void Engine::dev_pd_actions(const UuvPdGains& g, const void* ref6, void* act, cudaStream_t st) {
+    check_device();
+    if (fp64_)
+        cuda_check(Launch<double>::pd_actions(*pd_, g, (const double*)ref6, (double*)act, st),
+                   "dev_pd_actions");
+    else
+        cuda_check(Launch<float>::pd_actions(*pf_, g, (const float*)ref6, (float*)act, st),
+                   "dev_pd_actions");
+}
+
 void Engine::dev_states(void* out, cudaStream_t st) {
     check_device();
     if (fp64_) cuda_check(Launch<double>::pack_states_t(*pd_, (double*)out, st), "dev_states");

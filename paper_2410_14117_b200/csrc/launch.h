@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "uuv_common.cuh"
+#include "../../include/uuvsim.h"
 
 namespace uuv {
 
@@ -68,6 +69,8 @@ template <class T> struct Launch {
     static cudaError_t dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t st);
     static cudaError_t pack_states(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t pack_states_t(const EngineP<T>& p, T* out, cudaStream_t st);
+    static cudaError_t pd_actions(const EngineP<T>& p, const UuvPdGains& g, const T* ref, T* act,
+                                  cudaStream_t st);
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,

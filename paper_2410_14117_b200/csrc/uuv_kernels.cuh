@@ -591,6 +591,65 @@ __global__ void __launch_bounds__(BLOCK) k_dr_init(const __grid_constant__ Engin
     if (!ok) atomicMin(first_bad, e);
 }
 
+// PD baseline law over the state slab (reference baseline.py:38-75; restated in
+// paper_2410_14117_b200/baseline.py) -- one thread per env.
+// UuvPdGains in the engine precision (converted on the host per launch)
+template <class T> struct PdGainsT {
+    T kp[6], kd[6];
+    T pinv[2][8][6];
+    T kmax[2][8];
+    int32_t quadratic[2][8];
+};
+
+template <class T>
+__global__ void k_pd_actions(const __grid_constant__ EngineP<T> p,
+                             const __grid_constant__ PdGainsT<T> g, const T* __restrict__ ref,
+                             T* __restrict__ act) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= p.n_env) return;
+    const int slot = (p.n_veh > 1 && (int64_t)(p.env_offset + (uint64_t)e) >= p.mix_bound0) ? 1 : 0;
+    const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
+    const T s[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+    T sphi, cphi, sth, cth, spsi, cpsi;
+    if constexpr (is_f64<T>()) {
+        sincos(s[3], &sphi, &cphi); sincos(s[4], &sth, &cth); sincos(s[5], &spsi, &cpsi);
+    } else {
+        sincosf(s[3], &sphi, &cphi); sincosf(s[4], &sth, &cth); sincosf(s[5], &spsi, &cpsi);
+    }
+    const T R[3][3] = {
+        {cpsi * cth, -spsi * cphi + cpsi * sth * sphi, spsi * sphi + cpsi * cphi * sth},
+        {spsi * cth, cpsi * cphi + sphi * sth * spsi, -cpsi * sphi + sth * spsi * cphi},
+        {-sth, cth * sphi, cth * cphi}};
+    const T ew[3] = {ref[0] - s[0], ref[1] - s[1], ref[2] - s[2]};
+    T w[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {   // R^T ew
+        const T eb = R[0][j] * ew[0] + R[1][j] * ew[1] + R[2][j] * ew[2];
+        w[j] = g.kp[j] * eb - g.kd[j] * s[6 + j];
+    }
+    const T TWO_PI = Consts<T>::TWO_PI, PI = Consts<T>::PI;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {   // (a + pi) mod 2 pi - pi with floor-mod (Python %)
+        const T x = ref[3 + j] - s[3 + j] + PI;
+        const T ea = x - TWO_PI * floor(x / TWO_PI) - PI;
+        w[3 + j] = g.kp[3 + j] * ea - g.kd[3 + j] * s[9 + j];
+    }
+    const int nthr = p.veh[slot].n_thr;
+    T* out = act + (size_t)e * p.act_dim;
+    for (int i = 0; i < p.act_dim; ++i) {
+        T t = T(0);
+        if (i < nthr) {
+            T f = T(0);
+#pragma unroll
+            for (int j = 0; j < 6; ++j) f += g.pinv[slot][i][j] * w[j];
+            const T km = g.kmax[slot][i];
+            t = g.quadratic[slot][i] ? copysign(sqrt(fabs(f) / km), f) : f / km;
+            t = t > T(1) ? T(1) : (t < T(-1) ? T(-1) : t);
+        }
+        out[i] = t;
+    }
+}
+
 template <class T, class O = double>
 __global__ void k_pack_states(const __grid_constant__ EngineP<T> p, O* __restrict__ out) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -840,6 +899,24 @@ cudaError_t Launch<T>::dr_init(const EngineP<T>& p, int* first_bad, cudaStream_t
 template <class T>
 cudaError_t Launch<T>::pack_states(const EngineP<T>& p, double* out, cudaStream_t st) {
     k_pack_states<T, double><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, out);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::pd_actions(const EngineP<T>& p, const UuvPdGains& g, const T* ref, T* act,
+                                  cudaStream_t st) {
+    PdGainsT<T> gt;
+    for (int j = 0; j < 6; ++j) {
+        gt.kp[j] = (T)g.kp[j];
+        gt.kd[j] = (T)g.kd[j];
+    }
+    for (int v = 0; v < 2; ++v)
+        for (int i = 0; i < 8; ++i) {
+            for (int j = 0; j < 6; ++j) gt.pinv[v][i][j] = (T)g.pinv[v][i][j];
+            gt.kmax[v][i] = (T)g.kmax[v][i];
+            gt.quadratic[v][i] = g.quadratic[v][i];
+        }
+    k_pd_actions<T><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, gt, ref, act);
     return cudaGetLastError();
 }
 

@@ -230,3 +230,25 @@ def test_pd_graph_equals_eager():
         env.close()
     np.testing.assert_array_equal(res[0]["per_step_error"], res[1]["per_step_error"])
     np.testing.assert_array_equal(res[0]["dones"], res[1]["dones"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fused_pd_kernel_matches_torch_pd(precision):
+    spec = uuv.TaskSpec(kind="lemniscate")
+    params = uuv.bluerov2_params()
+    cfg = uuv.engine_config_dict(params, spec, 3000, 5, 0, uuv.default_ranges(per_episode=True),
+                                 precision=precision, device=0)
+    env = _gpu_env(cfg)
+    actor = B.PDActor(spec, params)
+    rng = np.random.default_rng(2)
+    s = env.states()
+    s[:, 3:6] = rng.uniform(-3.5, 3.5, (3000, 3))        # all headings, beyond +-pi
+    s[:, 6:12] = rng.normal(0, 0.5, (3000, 6))
+    env.set_states(s)
+    ref = torch.tensor([0.4, -0.3, 2.1, 0.2, -0.1, 3.0], dtype=env.dtype, device="cuda")
+    got = env.pd_actions_tensor(actor.engine_gains(), ref)
+    want = actor.act(env.states_tensor(), ref)
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    torch.testing.assert_close(got, want, rtol=tol, atol=tol)
+    env.close()
