@@ -24,7 +24,8 @@ constexpr int BLOCK = UUV_BLOCK;   // threads per block of the env kernels (one 
 #define UUV_STEP_MIN_BLOCKS_TRACK 6   // tracking (lookahead rows in registers): 85, no spills
 #endif
 #ifndef UUV_STEP_MIN_BLOCKS_F64
-#define UUV_STEP_MIN_BLOCKS_F64 4     // fp64 parity mode: 128 (doubles take register pairs;
+#define UUV_STEP_MIN_BLOCKS_F64 4     // fp64 parity mode and dense-pattern DR: 128 (doubles take
+                                      // register pairs; the dense DR kernel keeps a full M and L;
                                       // measured: C3 fp64 73.5 -> 45.5 us, C5 371 -> 400 us)
 #endif
 #ifndef UUV_PAIR_MIN_BLOCKS

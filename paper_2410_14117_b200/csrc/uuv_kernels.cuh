@@ -471,7 +471,7 @@ __device__ __forceinline__ void flush_obs(const EngineP<T>& p, void* __restrict_
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BLOCK, is_f64<T>() ? STEP_MIN_BLOCKS_F64
-                                      : (DR ? STEP_MIN_BLOCKS_DR
+                                      : (DR ? (Pat::fossen ? STEP_MIN_BLOCKS_DR : STEP_MIN_BLOCKS_F64)
                                             : (TRACK ? STEP_MIN_BLOCKS_TRACK : STEP_MIN_BLOCKS)))
 k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,

@@ -57,6 +57,7 @@ CONFIGS = {
     "mixed_station_dr": dict(mixed=True, dr="episode", episode_len=41),
     "mixed_circle_pair": dict(kind="circle", mixed=True, episode_len=33, pair="on", n=4000),
     "station_heavy_dense": dict(pattern="dense", episode_len=29),
+    "circle_dense_drep": dict(kind="circle", pattern="dense", dr="episode", episode_len=23),
 }
 
 
