@@ -52,8 +52,10 @@ __device__ __forceinline__ void stage(float* dst, const float* src, int rows, in
     for (int i = threadIdx.x; i < rows * c4; i += blockDim.x) {
         const int r = i / c4, c = (i - r * c4) * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c + 3 < cols) v = *reinterpret_cast<const float4*>(src + r * cols + c);
-        else if (c < cols) {
+        if ((cols & 3) == 0 && c + 3 < cols) {   // rows start 16-byte aligned
+            v = *reinterpret_cast<const float4*>(src + r * cols + c);
+        } else if (c < cols) {
+            if (c + 3 < cols) v.w = src[r * cols + c + 3];
             v.x = src[r * cols + c];
             if (c + 1 < cols) v.y = src[r * cols + c + 1];
             if (c + 2 < cols) v.z = src[r * cols + c + 2];

@@ -142,7 +142,7 @@ def _random_policy(obs_dim, act_dim, seed):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("tc", [False, True], ids=["cuda_cores", "tcgen05"])
-@pytest.mark.parametrize("obs_dim,act_dim", [(12, 6), (36, 8), (24, 6)])
+@pytest.mark.parametrize("obs_dim,act_dim", [(12, 6), (36, 8), (24, 6), (30, 3), (18, 1)])
 def test_fused_policy_matches_torch(obs_dim, act_dim, tc):
     from paper_2410_14117_b200.rl_fused import FusedActorCritic
     M = 1000
