@@ -825,7 +825,9 @@ void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* d
         abi_next_ = (abi_next_ + 1) % kAbiGraphs;
         if (g->exec) cudaGraphExecDestroy(g->exec);
         *g = AbiGraph{};
-        const bool zero_copy = mapped && use_mapped();
+        // zero-copy writes rows with 16-byte vector stores: require an aligned obs base
+        const bool zero_copy = mapped && use_mapped() && (((uintptr_t)obs & 15) == 0) &&
+                               (((uintptr_t)rew & 7) == 0) && (((uintptr_t)act & 7) == 0);
         cuda_check(cudaStreamSynchronize(stream_), "abi capture pre-sync");
         cudaGraph_t graph = nullptr;
         cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal),

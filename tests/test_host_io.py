@@ -135,3 +135,26 @@ def test_bench_throughput_and_bench_actions_match_reference_protocol():
     assert r["n_steps"] == 20 and r["num_envs"] == 1024 and r["threads"] == 4
     assert r["backend"] == "b200" and r["env_steps_per_sec"] > 0
     env.close()
+
+
+def test_mapped_transport_with_misaligned_pinned_buffers():
+    """A page-locked obs buffer that is only 8-byte aligned takes the DMA path
+    (zero-copy writes use 16-byte vector stores) and gives the same results."""
+    cfg = _cfg("lemniscate_dr", "mapped")
+    a = uuv.B200EnvBatch(cfg, 5, pinned=False)
+    b = uuv.B200EnvBatch(cfg, 5, pinned=False)
+    act = uuv.bench_actions(a)
+    n, d = a.num_envs, a.obs_dim
+    blk = torch.empty(n * d * 8 + 64, dtype=torch.uint8, pin_memory=True).numpy()
+    obs = blk[8:8 + n * d * 8].view(np.float64).reshape(n, d)       # base + 8 bytes
+    rew = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    done = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy()
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    for _ in range(CASES["lemniscate_dr"]["L"] + 3):
+        assert a._lib.uuvsim_step(a._handle, P(act), act.size, P(obs), obs.size, P(rew), n,
+                                  P(done), n) == 0
+        o, r, dn = b.step(act)
+        assert np.array_equal(obs, o) and np.array_equal(rew, r)
+        assert np.array_equal(done.astype(bool), dn)
+    a.close()
+    b.close()
