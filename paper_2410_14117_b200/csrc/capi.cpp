@@ -70,6 +70,13 @@ int32_t bad_size(const char* what, uint64_t want, const char* unit) {
 
 cudaStream_t as_stream(uint64_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// device-face output rows are written with 8/16-byte vector stores
+int32_t misaligned(const char* what, const void* p, uintptr_t align) {
+    if (((uintptr_t)p & (align - 1)) == 0) return UUVSIM_OK;
+    return fail(UUVSIM_ERR_SIZE, std::string(what) + " buffer must be " + std::to_string(align) +
+                                     "-byte aligned");
+}
+
 int64_t copy_out(const std::string& msg, char* buf, uint64_t cap) {
     if (buf && cap > 0) std::memcpy(buf, msg.data(), std::min<uint64_t>(cap, msg.size()));
     return (int64_t)msg.size();
@@ -249,6 +256,8 @@ int32_t uuvsim_dev_step(uint64_t h, const void* act, uint64_t act_len, void* obs
         if (!rew || rew_len != m) return bad_size("rewards", m, u);
         if (!done || done_len != m) return bad_size("dones", m, "u8");
         if (reason && reason_len != m) return bad_size("reasons", m, "i8");
+        if (int32_t c = misaligned("obs", obs, 16)) return c;
+        if (int32_t c = misaligned("actions", act, e.is_fp64() ? 8 : 4)) return c;
         e.dev_step(act, obs, rew, done, reason, as_stream(stream));
         return UUVSIM_OK;
     });
@@ -259,6 +268,9 @@ int32_t uuvsim_dev_reset(uint64_t h, uint64_t seed, void* obs, uint64_t obs_len,
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
         if (obs && obs_len != want) return bad_size("obs", want, e.is_fp64() ? "f64" : "f32");
+        if (obs) {
+            if (int32_t c = misaligned("obs", obs, 16)) return c;
+        }
         e.dev_reset(seed, obs, as_stream(stream));
         return UUVSIM_OK;
     });
@@ -268,6 +280,7 @@ int32_t uuvsim_dev_observe(uint64_t h, void* obs, uint64_t obs_len, uint64_t str
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
         if (!obs || obs_len != want) return bad_size("obs", want, e.is_fp64() ? "f64" : "f32");
+        if (int32_t c = misaligned("obs", obs, 16)) return c;
         e.dev_observe(obs, as_stream(stream));
         return UUVSIM_OK;
     });
@@ -331,6 +344,9 @@ int32_t uuvsim_dev_set_final_obs(uint64_t h, void* buf, uint64_t len) {
     return with_engine(h, [&](uuv::Engine& e) {
         const uint64_t want = (uint64_t)e.num_envs() * e.obs_dim();
         if (buf && len != want) return bad_size("final_obs", want, e.is_fp64() ? "f64" : "f32");
+        if (buf) {
+            if (int32_t c = misaligned("final_obs", buf, 16)) return c;
+        }
         e.dev_set_final_obs(buf);
         return UUVSIM_OK;
     });

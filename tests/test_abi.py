@@ -150,3 +150,19 @@ def test_reference_binding_loads_this_library(lib, monkeypatch):
     assert native.native_available()
     batch = importlib.import_module("uuvsim.batch")
     assert batch.resolve_backend() == "native"
+
+
+@pytest.mark.gpu
+def test_device_face_rejects_misaligned_rows():
+    import torch
+    env = uuv.B200EnvBatch(uuv.engine_config_dict(uuv.default_params(), uuv.TaskSpec(), 64, 0,
+                                                  device=0))
+    lib, h = env._lib, env._handle
+    n, d = env.num_envs, env.obs_dim
+    raw = torch.empty(n * d + 4, dtype=torch.float32, device="cuda")
+    bad = raw[1:1 + n * d]                      # 4-byte offset: not 16-byte aligned
+    assert lib.uuvsim_dev_observe(h, bad.data_ptr(), bad.numel(), 0) == 3
+    assert "16-byte aligned" in uuv._core.last_error(lib)
+    good = raw[4:4 + n * d]
+    assert lib.uuvsim_dev_observe(h, good.data_ptr(), good.numel(), 0) == 0
+    env.close()
