@@ -264,6 +264,11 @@ void Engine::parse(const std::string& text) {
     if (task_.kind == 3 && !(task_.scale > 0.0)) throw ConfigError("scale must be positive");
     if (task_.episode_len > (int64_t)INT32_MAX - task_.lookahead - 2)
         throw ConfigError("episode_len too large for the device step counter (int32)");
+    // tracking references come from a per-step table (host fp64 -> device): bound it
+    // (2^26 rows = 39 days of simulated time per episode at 0.05 s)
+    if (task_.kind != 0 && task_.episode_len + task_.lookahead + 1 > (int64_t)1 << 26)
+        throw ConfigError("tracking tasks support episode_len + lookahead up to 67108863 "
+                          "(device trajectory table)");
 
     // batch (engine.rs:406-417)
     json b = json::object();

@@ -95,6 +95,8 @@ BASE = uuv.engine_config_dict(uuv.default_params(), uuv.TaskSpec(), 16, 0)
     (lambda c: c["task"].update(kind="lemniscate", scale=-1.0), "scale must be positive"),
     (lambda c: c["batch"].__setitem__("num_envs", 0), "batch.num_envs must be >= 1"),
     (lambda c: c["batch"].__setitem__("num_envs", 1 << 31), "too large for one device slab"),
+    (lambda c: c["task"].update(kind="circle", episode_len=1 << 27), "device trajectory table"),
+    (lambda c: c["task"].__setitem__("episode_len", 1 << 31), "too large for the device step counter"),
     (lambda c: c["batch"].__setitem__("randomization", {"mass": [1.2, 1.1]}),
      "range mass must satisfy 0 < lo <= hi"),
     (lambda c: c["batch"].__setitem__("randomization", {"rb_offset": -1.0}),
