@@ -71,7 +71,10 @@ class B200EnvBatch:
                 pass
         self._t = None          # device tensors (lazy)
         self._bufptrs = None
-        self.reset_all(self.root_seed)
+        if self.root_seed != int(cfg["seed"]):
+            self.reset_all(self.root_seed)
+        # else: the engine reset every env with the config seed at create; skipping
+        # the host reset keeps a device-face-only batch free of host-ABI staging
 
     # -------------------------------------------------------------- reference protocol
     def reset_all(self, seed: int) -> np.ndarray:

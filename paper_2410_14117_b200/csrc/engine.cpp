@@ -542,10 +542,10 @@ void Engine::allocate() {
     if (ranges_.enabled) bytes += 2 * align256(N * 4 * sT) + align256(N * 2 * sT);
     size_t free_b = 0, total_b = 0;
     cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const size_t abi = (align256(N * n_act_ * 8) + align256(N * obs_dim_ * 8) + align256(N * 8)) *
-                           (fp64_ ? 1 : 2) + 2 * align256(N) + align256(N * 12 * 8);
-    if (bytes + abi > free_b)
-        throw ConfigError("batch.num_envs needs " + std::to_string((bytes + abi) >> 20) +
+    // the host-ABI staging buffers are allocated on first use (ensure_staging):
+    // a device-face user (uuvsim_dev_*) never pays for them
+    if (bytes > free_b)
+        throw ConfigError("batch.num_envs needs " + std::to_string(bytes >> 20) +
                           " MiB of device memory, " + std::to_string(free_b >> 20) + " MiB free");
     arena_bytes_ = bytes;
     cuda_check(cudaMalloc(&arena_, bytes), "cudaMalloc(state)");
@@ -567,21 +567,6 @@ void Engine::allocate() {
             cuda_check(cudaMemcpy(traj_, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice), "traj");
         }
     }
-    cuda_check(cudaMalloc(&d_act64_, N * n_act_ * 8), "cudaMalloc(abi act)");
-    cuda_check(cudaMalloc(&d_obs64_, N * obs_dim_ * 8), "cudaMalloc(abi obs)");
-    cuda_check(cudaMalloc(&d_rew64_, N * 8), "cudaMalloc(abi rew)");
-    if (fp64_) {
-        d_actT_ = d_act64_;
-        d_obsT_ = d_obs64_;
-        d_rewT_ = d_rew64_;
-    } else {
-        cuda_check(cudaMalloc(&d_actT_, N * n_act_ * 4), "cudaMalloc(abi act32)");
-        cuda_check(cudaMalloc(&d_obsT_, N * obs_dim_ * 4), "cudaMalloc(abi obs32)");
-        cuda_check(cudaMalloc(&d_rewT_, N * 4), "cudaMalloc(abi rew32)");
-    }
-    cuda_check(cudaMalloc(&d_done_, N), "cudaMalloc(abi done)");
-    cuda_check(cudaMalloc(&d_reason_, N), "cudaMalloc(abi reason)");
-    cuda_check(cudaMalloc(&d_pack_, N * 12 * 8), "cudaMalloc(abi pack)");
     cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "cudaMalloc(flag)");
     {   // fp32 register pack per vehicle (uuv_model.cuh RegPack layout)
         std::vector<float> pk((size_t)MAX_VEH * PACK_F4 * 4, 0.0f);
@@ -612,6 +597,64 @@ void Engine::allocate() {
                    "vpack");
     }
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+// host-ABI staging (f64 action / obs / reward rows, fp32 twins, done / reason
+// bytes), allocated the first time a host-face call needs it
+void Engine::ensure_staging() {
+    if (d_act64_) return;
+    const size_t N = (size_t)m_;
+    const size_t need = (align256(N * n_act_ * 8) + align256(N * obs_dim_ * 8) + align256(N * 8)) *
+                            (fp64_ ? 1 : 2) + 2 * align256(N);
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    if (need > free_b)
+        throw ConfigError("the host-ABI staging for batch.num_envs needs " +
+                          std::to_string(need >> 20) + " MiB of device memory, " +
+                          std::to_string(free_b >> 20) +
+                          " MiB free (the device face uuvsim_dev_* needs none)");
+    try {
+        cuda_check(cudaMalloc(&d_act64_, N * n_act_ * 8), "cudaMalloc(abi act)");
+        cuda_check(cudaMalloc(&d_obs64_, N * obs_dim_ * 8), "cudaMalloc(abi obs)");
+        cuda_check(cudaMalloc(&d_rew64_, N * 8), "cudaMalloc(abi rew)");
+        if (fp64_) {
+            d_actT_ = d_act64_;
+            d_obsT_ = d_obs64_;
+            d_rewT_ = d_rew64_;
+        } else {
+            cuda_check(cudaMalloc(&d_actT_, N * n_act_ * 4), "cudaMalloc(abi act32)");
+            cuda_check(cudaMalloc(&d_obsT_, N * obs_dim_ * 4), "cudaMalloc(abi obs32)");
+            cuda_check(cudaMalloc(&d_rewT_, N * 4), "cudaMalloc(abi rew32)");
+        }
+        cuda_check(cudaMalloc(&d_done_, N), "cudaMalloc(abi done)");
+        cuda_check(cudaMalloc(&d_reason_, N), "cudaMalloc(abi reason)");
+    } catch (...) {
+        free_staging();
+        throw;
+    }
+    staging_bytes_ = need;
+}
+
+// [N][12] f64 state rows for the host state accessors
+void Engine::ensure_pack() {
+    if (d_pack_) return;
+    cuda_check(cudaMalloc(&d_pack_, (size_t)m_ * 12 * 8), "cudaMalloc(abi pack)");
+}
+
+void Engine::free_staging() {
+    if (!fp64_) {
+        void* t[] = {d_actT_, d_obsT_, d_rewT_};
+        for (void* b : t)
+            if (b) cudaFree(b);
+    }
+    void* bufs[] = {d_act64_, d_obs64_, d_rew64_, d_done_, d_reason_};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    d_actT_ = d_obsT_ = d_rewT_ = nullptr;
+    d_act64_ = d_obs64_ = d_rew64_ = nullptr;
+    d_done_ = nullptr;
+    d_reason_ = nullptr;
+    staging_bytes_ = 0;
 }
 
 Engine::Engine(const std::string& text) {
@@ -646,20 +689,12 @@ void Engine::release() {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g = AbiGraph{};
     }
-    if (!fp64_) {
-        void* t[] = {d_actT_, d_obsT_, d_rewT_};
-        for (void* b : t)
-            if (b) cudaFree(b);
-    }
-    d_actT_ = d_obsT_ = d_rewT_ = nullptr;
-    void* bufs[] = {arena_, traj_, stats_part_, d_act64_, d_obs64_, d_rew64_, d_done_,
-                    d_reason_, d_pack_, d_flag_, d_stats_out_, d_vpack_};
+    free_staging();
+    void* bufs[] = {arena_, traj_, stats_part_, d_pack_, d_flag_, d_stats_out_, d_vpack_};
     for (void* b : bufs)
         if (b) cudaFree(b);
     arena_ = traj_ = nullptr;
-    stats_part_ = d_act64_ = d_obs64_ = d_rew64_ = d_pack_ = d_stats_out_ = nullptr;
-    d_done_ = nullptr;
-    d_reason_ = nullptr;
+    stats_part_ = d_pack_ = d_stats_out_ = nullptr;
     d_flag_ = nullptr;
     d_vpack_ = nullptr;
     if (stream_) cudaStreamDestroy(stream_);
@@ -683,6 +718,7 @@ void Engine::init_randomization() {   // engine.rs:440-458: per-env sample at cr
 
 // ------------------------------------------------------------------ host ABI face
 template <class T> void Engine::reset_host_T(uint64_t seed, double* obs) {
+    if (obs) ensure_staging();
     EngineP<T>& p = P<T>();
     p.seed = seed;
     const size_t n_obs = (size_t)m_ * obs_dim_;
@@ -813,6 +849,7 @@ void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* d
         dev_io_[i] = hb[i].dev;
     }
     if (!locked) {   // pageable buffers: staged DMA, no graph
+        ensure_staging();
         enqueue_step_host<T>(act, obs, rew, done, reason);
         cuda_check(cudaStreamSynchronize(stream_), "step sync");
         return;
@@ -833,6 +870,7 @@ void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* d
         // zero-copy writes rows with 16-byte vector stores: require an aligned obs base
         const bool zero_copy = mapped && use_mapped() && (((uintptr_t)obs & 15) == 0) &&
                                (((uintptr_t)rew & 7) == 0) && (((uintptr_t)act & 7) == 0);
+        if (!zero_copy) ensure_staging();   // no allocation inside the capture
         cuda_check(cudaStreamSynchronize(stream_), "abi capture pre-sync");
         cudaGraph_t graph = nullptr;
         cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal),
@@ -867,6 +905,7 @@ void Engine::step_host(const double* act, double* obs, double* rew, uint8_t* don
 
 void Engine::states_host(double* out) {
     activate();
+    ensure_pack();
     if (fp64_) cuda_check(Launch<double>::pack_states(*pd_, d_pack_, stream_), "pack");
     else cuda_check(Launch<float>::pack_states(*pf_, d_pack_, stream_), "pack");
     cuda_check(cudaMemcpyAsync(out, d_pack_, (size_t)m_ * 12 * 8, cudaMemcpyDeviceToHost, stream_), "states D2H");
@@ -875,6 +914,7 @@ void Engine::states_host(double* out) {
 
 void Engine::set_states_host(const double* in) {
     activate();
+    ensure_pack();
     cuda_check(cudaMemcpyAsync(d_pack_, in, (size_t)m_ * 12 * 8, cudaMemcpyHostToDevice, stream_), "states H2D");
     if (fp64_) cuda_check(Launch<double>::unpack_states(*pd_, d_pack_, stream_), "unpack");
     else cuda_check(Launch<float>::unpack_states(*pf_, d_pack_, stream_), "unpack");
@@ -924,6 +964,7 @@ void Engine::dr_factors_host(double* out) {
         }
         return;
     }
+    ensure_pack();
     if (fp64_) cuda_check(Launch<double>::pack_dr(*pd_, d_pack_, stream_), "pack_dr");
     else cuda_check(Launch<float>::pack_dr(*pf_, d_pack_, stream_), "pack_dr");
     cuda_check(cudaMemcpyAsync(out, d_pack_, (size_t)m_ * 10 * 8, cudaMemcpyDeviceToHost, stream_), "dr D2H");
@@ -1147,6 +1188,7 @@ std::string Engine::info() const {
         {"host_io", host_io_ == 0 ? "copy" : host_io_ == 1 ? "mapped" : "auto"},
         {"arena_address", (uint64_t)(uintptr_t)arena_},
         {"arena_bytes", (uint64_t)arena_used_},
+        {"abi_staging_bytes", (uint64_t)(staging_bytes_ + (d_pack_ ? (size_t)m_ * 96 : 0))},
         {"per_episode", ranges_.per_episode},
         {"device", device_},
         {"device_name", device_name_},

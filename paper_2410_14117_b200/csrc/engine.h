@@ -114,6 +114,9 @@ private:
     void release();
     void build_params();
     void allocate();
+    void ensure_staging();
+    void ensure_pack();
+    void free_staging();
     void init_randomization();
     template <class T> EngineP<T>& P();
     template <class T> void fill_params(EngineP<T>& p);
@@ -148,6 +151,7 @@ private:
     // device memory
     void* arena_ = nullptr;
     size_t arena_bytes_ = 0;
+    size_t staging_bytes_ = 0;   // host-ABI staging, allocated on first host-face use
     size_t arena_used_ = 0;   // per-env state occupies arena_[0, arena_used_)
     uint64_t config_hash() const;
     void* traj_ = nullptr;

@@ -145,7 +145,7 @@ def test_tiny_and_ragged_batches(n):
 def test_slab_beyond_device_memory_is_a_config_error():
     import ctypes
     import json
-    cfg = _cfg(n=1 << 30)                       # ~300 GB with staging: cannot fit
+    cfg = _cfg(n=(1 << 31) - 4096, precision="fp64")   # ~257 GB of fp64 state: cannot fit
     lib = uuv._core.load()
     h = ctypes.c_uint64(0)
     code = lib.uuvsim_create(json.dumps(cfg).encode(), ctypes.byref(h))
@@ -155,7 +155,7 @@ def test_slab_beyond_device_memory_is_a_config_error():
 
 @pytest.mark.slow
 def test_maximum_slab_high_indices_exact():
-    """2^27 envs (~45 GB with the ABI staging): the last envs of the slab reset
+    """2^27 envs (~10 GB of state, +13 GB of host state rows): the last envs of the slab reset
     exactly like the oracle's envs at the same global index, and a step touches
     every env (64-bit row offsets everywhere)."""
     n = 1 << 27
@@ -176,3 +176,47 @@ def test_maximum_slab_high_indices_exact():
     assert int(g.step_counts()[-1]) == 2
     o.close()
     g.close()
+
+
+def test_host_staging_is_allocated_on_first_host_use():
+    """The device face needs no host-ABI staging: an engine driven only through
+    uuvsim_dev_* never allocates it; the first host-face call does."""
+    import ctypes
+    import json
+    n = 4096
+    cfg = _cfg(n=n)
+    lib = uuv._core.load()
+    h = ctypes.c_uint64(0)
+    assert lib.uuvsim_create(json.dumps(cfg).encode(), ctypes.byref(h)) == 0
+
+    def staging():
+        buf = ctypes.create_string_buffer(1 << 16)
+        assert lib.uuvsim_info(h, buf, len(buf)) > 0
+        return json.loads(buf.value.decode())["abi_staging_bytes"]
+
+    try:
+        spec = (ctypes.c_uint64 * 4)()
+        assert lib.uuvsim_spec(h, spec) == 0
+        od, ad = int(spec[1]), int(spec[2])
+        assert staging() == 0
+        a = torch.zeros((n, ad), device="cuda")
+        o = torch.empty((n, od), device="cuda")
+        r = torch.empty(n, device="cuda")
+        d = torch.empty(n, dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        assert lib.uuvsim_dev_step(h, a.data_ptr(), a.numel(), o.data_ptr(), o.numel(),
+                                   r.data_ptr(), n, d.data_ptr(), n, None, 0, st) == 0
+        torch.cuda.synchronize()
+        assert staging() == 0
+        s = np.empty((n, 12))
+        assert lib.uuvsim_states(h, s.ctypes.data, s.size) == 0
+        assert staging() == n * 96                 # state rows only
+        act = np.zeros((n, ad))
+        obs, rew = np.empty((n, od)), np.empty(n)
+        done = np.empty(n, dtype=np.uint8)
+        assert lib.uuvsim_step(h, act.ctypes.data, act.size, obs.ctypes.data, obs.size,
+                               rew.ctypes.data, n, done.ctypes.data, n) == 0
+        assert staging() > n * 96
+        assert np.isfinite(obs).all()
+    finally:
+        lib.uuvsim_destroy(h)
