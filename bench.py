@@ -43,6 +43,11 @@ CONFIGS = {
                vehicles=["bluerov2"], num_envs=4096, dr=None),
     "c3": dict(workload="C3 BlueROV2-Heavy lemniscate tracking + per-episode DR, 65536 envs/GPU",
                kind="lemniscate", vehicles=["bluerov2_heavy"], num_envs=65536, dr="episode"),
+    # lemniscate is the headline, circle and helix are also reported
+    "c3_circle": dict(workload="C3 BlueROV2-Heavy circle tracking + per-episode DR, 65536 envs/GPU",
+                      kind="circle", vehicles=["bluerov2_heavy"], num_envs=65536, dr="episode"),
+    "c3_helix": dict(workload="C3 BlueROV2-Heavy helix tracking + per-episode DR, 65536 envs/GPU",
+                     kind="helix", vehicles=["bluerov2_heavy"], num_envs=65536, dr="episode"),
     "c4": dict(workload="C4 BlueROV2 circle tracking, 16384 envs/GPU", kind="circle",
                vehicles=["bluerov2"], num_envs=16384, dr=None),
     "c5": dict(workload="C5 mixed BlueROV2/Heavy station-keeping, 1048576 envs/GPU",
@@ -440,7 +445,7 @@ def main():
         sweep = []
         del env
         torch.cuda.empty_cache()
-        for name in ("c4", "c3", "c5"):
+        for name in ("c4", "c3", "c3_circle", "c3_helix", "c5"):
             if name == args.config:
                 continue
             cfg2, nt2 = build_config(name, rank, args.precision, args.pair, args.stage_obs)
