@@ -24,6 +24,7 @@ from paper_2410_14117_b200 import _core
 
 ROOT = Path(__file__).resolve().parent.parent
 HEADER = ROOT / "include" / "uuvsim.h"
+HEADERS = sorted((ROOT / "include").glob("*.h"))
 
 
 @pytest.fixture(scope="module")
@@ -33,13 +34,18 @@ def lib():
     return _core.load()
 
 
-def _declared_symbols():
-    return sorted(set(re.findall(r"\b(uuvsim_\w+)\s*\(", HEADER.read_text())))
+def _declared_symbols(headers=None):
+    text = "".join(h.read_text() for h in (headers or HEADERS))
+    return sorted(set(re.findall(r"\b(uuvsim_\w+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol(lib):
+    """Every function any header under include/ declares (uuvsim.h: the ABI v1 +
+    device face; uuvsim_rl.h: the rollout-loop kernels) is exported."""
+    assert {h.name for h in HEADERS} >= {"uuvsim.h", "uuvsim_rl.h"}
     syms = _declared_symbols()
-    assert len(syms) >= 25
+    assert len(syms) >= 30
+    assert "uuvsim_rl_policy_act" in syms and "uuvsim_rl_gae" in syms
     for name in syms:
         assert hasattr(lib, name), name
     # the ten ABI-v1 symbols the reference binds (reference _native.py:49-78)
