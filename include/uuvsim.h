@@ -119,6 +119,14 @@ int32_t uuvsim_restore(uint64_t handle, const void* buf, uint64_t len);
  * env's TERMINAL observation (pre-reset state, terminating step) into its row;
  * other rows are left untouched.  Not used by the host-buffer uuvsim_step. */
 int32_t uuvsim_dev_set_final_obs(uint64_t handle, void* buf, uint64_t len);
+/* on != 0: later device-face steps launch as programmatic dependents of the
+ * previous kernel on their stream (griddepcontrol: the step's CTAs may be
+ * scheduled while that kernel finishes and wait for its completion before
+ * reading anything; they also let the next programmatic dependent launch
+ * early).  Inside a CUDA graph of back-to-back kernels this hides the
+ * kernel-to-kernel launch gap.  Results are unchanged.  Host-ABI steps never
+ * use it. */
+int32_t uuvsim_dev_set_pdl(uint64_t handle, int32_t on);
 /* PD baseline (reference baseline.py:38-75) over the engine's own state slab:
  * err_body = R^T (ref_xyz - p), err_ang = (ref_ang - ang + pi) mod 2 pi - pi,
  * wrench = kp * err - kd * nu, f = pinv(A) wrench, throttle = f / kmax (linear) or

@@ -37,7 +37,9 @@ typedef struct {
     uint32_t act_dim;        /* <= 8 */
     uint32_t hidden;         /* 64 */
     uint32_t flags;          /* 1: sample (else act = raw = mean), 2: accumulate normaliser sums,
-                                4: value only (bootstrap) */
+                                4: value only (bootstrap), 8: launch as a programmatic dependent
+                                of the previous kernel on the stream (tensor-core kernel; see
+                                uuvsim_dev_set_pdl) */
     uint64_t seed;           /* noise stream seed */
     uint64_t env_offset;     /* global index of env 0 (noise stream id) */
     const uint64_t* noise_ctr;   /* device counter, advanced by uuvsim_rl_post */
@@ -72,6 +74,8 @@ typedef struct {
     float* rew_out;
     float* done_out;
     uint64_t* noise_ctr;     /* += 1 */
+    uint32_t flags;          /* 1: launch as a programmatic dependent of the previous kernel */
+    uint32_t reserved;
 } UuvRlPostArgs;
 
 /* partial rows the policy launch writes for num_envs (size of stats_part / (2 D)) */

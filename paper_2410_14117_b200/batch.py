@@ -292,6 +292,12 @@ class B200EnvBatch:
             self._stream(stream)))
         return t["obs"], t["rew"], t["done"], t["reason"]
 
+    def set_pdl(self, on: bool = True) -> None:
+        """Launch later device-face steps as programmatic dependents of the previous
+        kernel on the stream (include/uuvsim.h uuvsim_dev_set_pdl); results unchanged."""
+        self._require_open()
+        _core.check(self._lib, self._lib.uuvsim_dev_set_pdl(self._handle, 1 if on else 0))
+
     def observe_tensors(self, stream=None):
         t = self._tensors()
         _core.check(self._lib, self._lib.uuvsim_dev_observe(

@@ -352,6 +352,13 @@ int32_t uuvsim_dev_set_final_obs(uint64_t h, void* buf, uint64_t len) {
     });
 }
 
+int32_t uuvsim_dev_set_pdl(uint64_t h, int32_t on) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        e.dev_set_pdl(on != 0);
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_stats(uint64_t h, double* out, uint64_t len, int32_t clear, uint64_t stream) {
     return with_engine(h, [&](uuv::Engine& e) {
         if (!out || len != (uint64_t)uuv::NSTAT) return bad_size("stats", uuv::NSTAT, "f64");

@@ -747,13 +747,16 @@ void Engine::enqueue_step_host(const double* act, double* obs, double* rew, uint
                "step H2D");
     EngineP<T>& p = P<T>();
     p.io_f64 = 1;
-    void* const fo = p.final_obs;   // terminal obs: device face only
+    void* const fo = p.final_obs;   // terminal obs and programmatic launch: device face only
+    const int32_t pdl = p.pdl;
     p.final_obs = nullptr;
+    p.pdl = 0;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           d_act64_, d_obs64_, d_rew64_, d_done_, d_reason_,
                                           stream_);
     p.io_f64 = fp64_ ? 1 : 0;
     p.final_obs = fo;
+    p.pdl = pdl;
     cuda_check(e, "step");
     cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
     cuda_check(cudaMemcpyAsync(rew, d_rew64_, N * 8, cudaMemcpyDeviceToHost, stream_), "rew D2H");
@@ -819,10 +822,11 @@ HostBuf host_buf(const void* ptr) {
 template <class T>
 void Engine::enqueue_step_mapped() {
     EngineP<T>& p = P<T>();
-    const int32_t io = p.io_f64, stage = p.stage_obs;
+    const int32_t io = p.io_f64, stage = p.stage_obs, pdl = p.pdl;
     void* const fo = p.final_obs;
     p.io_f64 = 1;
     p.final_obs = nullptr;
+    p.pdl = 0;
     p.stage_obs = obs_dim_ <= MAX_STAGE_DIM ? 1 : 0;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           dev_io_[0], dev_io_[1], dev_io_[2],
@@ -831,6 +835,7 @@ void Engine::enqueue_step_mapped() {
     p.io_f64 = io;
     p.stage_obs = stage;
     p.final_obs = fo;
+    p.pdl = pdl;
     cuda_check(e, "step (mapped)");
 }
 
@@ -1092,6 +1097,11 @@ void Engine::dev_observe(void* obs, cudaStream_t st) {
     check_device();
     if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
+}
+
+void Engine::dev_set_pdl(bool on) {
+    if (fp64_) pd_->pdl = on ? 1 : 0;
+    else pf_->pdl = on ? 1 : 0;
 }
 
 void Engine::dev_set_final_obs(void* buf) {

@@ -37,6 +37,14 @@ constexpr int PAIR_MIN_BLOCKS = UUV_PAIR_MIN_BLOCKS;
 constexpr int STEP_MIN_BLOCKS_TRACK = UUV_STEP_MIN_BLOCKS_TRACK;
 constexpr int STEP_MIN_BLOCKS_F64 = UUV_STEP_MIN_BLOCKS_F64;
 
+#ifndef UUV_PDL_TRIGGER
+#define UUV_PDL_TRIGGER 0          // programmatic launch: 0 implicit trigger at completion,
+                                   // 1 at kernel start, 2 after the heavy work.  Measured on
+                                   // the C4 loop (us per step): 31.8 / 38.9 / 37.6, no PDL
+                                   // 33.0 -- resident dependents waiting in griddepcontrol
+                                   // slow the running kernel more than the launch they save
+#endif
+
 #ifndef UUV_PAIR_AUTO_MIN_ENVS
 #define UUV_PAIR_AUTO_MIN_ENVS 131072
 #endif

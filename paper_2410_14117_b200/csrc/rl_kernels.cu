@@ -14,6 +14,10 @@
 #include "uuv_common.cuh"
 #include "../../include/uuvsim_rl.h"
 
+#ifndef UUV_PDL_TRIGGER
+#define UUV_PDL_TRIGGER 0   // explicit dependents trigger: off (see launch.h)
+#endif
+
 namespace uuvrl {
 
 // Work split: a block holds 64 envs and 8 warps; warp w works on env half w >> 2
@@ -256,6 +260,10 @@ __global__ void __launch_bounds__(BLK, 2) k_policy_act(const UuvRlPolicyArgs a) 
 }
 
 __global__ void k_rl_post(const UuvRlPostArgs a) {
+    if (a.flags & 1) {   // programmatic dependent launch (see k_policy_tc)
+        if (UUV_PDL_TRIGGER >= 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < a.num_envs) {
         if (a.rew_in && a.rew_out) a.rew_out[e] = a.rew_in[e];
@@ -267,26 +275,41 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
     const int D = (int)a.obs_dim;
     const double n = (double)a.num_envs;
     if (a.n_part > 0) {   // RunningNorm.update: parallel-variance merge (nets.py:177-188)
-        // one warp per (sum, dim) column: lanes stride the partial rows, then a
-        // fixed shuffle tree -- deterministic and ~n_part/32 dependent loads deep
+        // the running statistics are read up front (one round trip with the sums)
+        const bool owner = (int)threadIdx.x < D;
+        const double cnt = *a.norm_count;
+        const double m = owner ? a.norm_mean[threadIdx.x] : 0.0;
+        const double v = owner ? a.norm_var[threadIdx.x] : 0.0;
+        // one warp per (sum, dim) column (2 D <= 72 columns: at most 3 per warp of
+        // a 1024-thread block): lanes stride the partial rows, every load of all of
+        // the warp's columns in flight together, then a fixed shuffle tree --
+        // deterministic
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        for (int col = warp; col < 2 * D; col += nw) {
-            double v = 0.0;
+        constexpr int CPW = 3;
+        double acc[CPW] = {0.0, 0.0, 0.0};
 #pragma unroll 8
-            for (uint32_t b = lane; b < a.n_part; b += 32) v += a.stats_part[(size_t)b * 2 * D + col];
+        for (uint32_t b = lane; b < a.n_part; b += 32) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) sums[col] = v;
+            for (int c = 0; c < CPW; ++c) {
+                const int col = warp + c * nw;
+                if (col < 2 * D) acc[c] += a.stats_part[(size_t)b * 2 * D + col];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            double x = acc[c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            const int col = warp + c * nw;
+            if (lane == 0 && col < 2 * D) sums[col] = x;
         }
         __syncthreads();
-        const double cnt = *a.norm_count;
         const double tot = cnt + n;
-        if ((int)threadIdx.x < D) {
+        if (owner) {
             const int d = threadIdx.x;
             const double s = sums[d], q = sums[D + d];
             const double bm = s / n;
             const double bv = fmax(q / n - bm * bm, 0.0);
-            const double m = a.norm_mean[d], v = a.norm_var[d];
             const double delta = bm - m;
             const double m2 = v * cnt + bv * n + delta * delta * (cnt * n / tot);
             a.norm_mean[d] = m + delta * (n / tot);
@@ -297,6 +320,27 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
         if (threadIdx.x == 0) *a.norm_count = tot_sh;
     }
     if (threadIdx.x == 0 && a.noise_ctr) *a.noise_ctr += 1;
+}
+
+// <<<>>> launch, or cudaLaunchKernelEx with programmatic stream serialisation
+template <class... KArgs, class... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t st, bool pdl, Args... args) {
+    if (!pdl) {
+        k<<<grid, block, smem, st>>>(args...);
+        return cudaSuccess;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 // dynamic shared memory opt-in, once per kernel and device (attributes are per
@@ -527,21 +571,26 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int row = ((warp & 3) << 5) + lane;            // env in CTA = TMEM lane
     const int ch = warp >> 2;                            // column half
+    const bool pdl = (a.flags & 8) != 0;                 // programmatic dependent launch
+    if (pdl && UUV_PDL_TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < D) {
-        nsc[tid] = a.norm_mean[tid];
-        nsc[36 + tid] = 1.0 / sqrt(a.norm_var[tid] + 1e-8);
-    }
-    __syncwarp();
     if (warp == 0) {   // 64 TMEM columns: one fp32 128 x 64 accumulator
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;"
                      ::"r"(s_u32(&tmem_base_sh)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // everything above overlaps the predecessor's tail; nothing it writes
+    // (observations, normaliser statistics, noise counter, weight image) is read
+    // before this point
+    if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid < D) {
+        nsc[tid] = a.norm_mean[tid];
+        nsc[36 + tid] = 1.0 / sqrt(a.norm_var[tid] + 1e-8);
     }
     tc_fence_before();
     __syncthreads();
@@ -555,24 +604,72 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
             ::"r"(s_u32(wimg)), "l"(a.wimage), "r"(g.total), "r"(s_u32(&bars[0])) : "memory");
     }
 
-    // ---- observations (column half 0): normaliser sums, normalise + clip, A_z, nobs_out
+    // ---- observations: normaliser sums, normalise + clip, A_z, nobs_out
     const uint64_t e = (uint64_t)blockIdx.x * M + row;
     const bool active = e < a.num_envs;
+    const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;   // issued early: one round trip
     float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][37] (A_h unused yet)
-    if (ch == 0) {
-#pragma unroll 4
-        for (int k = 0; k < D; ++k) raw[row * 37 + k] = active ? __ldg(a.obs + e * D + k) : 0.0f;
+    const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
+    const int nvalid = left < (uint64_t)M ? (int)left : M;
+    {   // the CTA's rows are one contiguous span: coalesced 16-byte loads by every
+        // thread, all issued before any shared-memory store (one memory round trip)
+        const float* src = a.obs + (uint64_t)blockIdx.x * M * D;
+        const int nf = nvalid * D;
+        constexpr int PER = (M * 36 / 4 + NT - 1) / NT;   // float4 per thread at D = 36
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const int n4 = nf >> 2;
+            float4 buf[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid + j * NT;
+                buf[j] = i < n4 ? __ldg(reinterpret_cast<const float4*>(src) + i) : float4{};
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int i = tid + j * NT;
+                if (i < n4) {
+                    const float* bv = &buf[j].x;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int f = 4 * i + t, r = f / D;
+                        raw[r * 37 + (f - r * D)] = bv[t];
+                    }
+                }
+            }
+            for (int f = (n4 << 2) + tid; f < nf; f += NT) {
+                const int r = f / D;
+                raw[r * 37 + (f - r * D)] = __ldg(src + f);
+            }
+        } else {
+            for (int f = tid; f < nf; f += NT) {
+                const int r = f / D;
+                raw[r * 37 + (f - r * D)] = __ldg(src + f);
+            }
+        }
+        for (int f = nf + tid; f < M * D; f += NT) {   // rows past the last env
+            const int r = f / D;
+            raw[r * 37 + (f - r * D)] = 0.0f;
+        }
     }
     __syncthreads();
     if ((a.flags & 2) && tid < 2 * D) {
         const int d = tid < D ? tid : tid - D;
-        const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
-        const int nvalid = left < (uint64_t)M ? (int)left : M;
-        double acc = 0.0;
-        for (int r = 0; r < nvalid; ++r) {
-            const double v = raw[r * 37 + d];
-            acc += tid < D ? v : v * v;
+        // four interleaved partial sums (fixed order: deterministic) shorten the
+        // fp64 dependency chain 4x
+        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+        int r = 0;
+        for (; r + 4 <= nvalid; r += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double v = raw[(r + q) * 37 + d];
+                acc4[q] += tid < D ? v : v * v;
+            }
         }
+        for (; r < nvalid; ++r) {
+            const double v = raw[r * 37 + d];
+            acc4[0] += tid < D ? v : v * v;
+        }
+        const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
         const uint32_t row2 = 2u * blockIdx.x;
         a.stats_part[(size_t)row2 * 2 * D + tid] = acc;
         a.stats_part[(size_t)(row2 + 1) * 2 * D + tid] = 0.0;   // FFMA-kernel granularity
@@ -672,6 +769,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     }
     tc_fence_before();
     __syncthreads();
+    if (UUV_PDL_TRIGGER == 2 && pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
     if (value_only) {
@@ -679,7 +777,6 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         return;
     }
     // action dims: half ch takes Box-Muller pairs 2 ch and 2 ch + 1 (dims 4 ch .. 4 ch + 3)
-    const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;
     const uint64_t gid = a.env_offset + e;
     float logp = 0.0f;
 #pragma unroll 1
@@ -800,8 +897,9 @@ int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* a, uint64_t stream) {
         const size_t smem = uuvtc::smem_bytes((int)a->obs_dim);
         uuvrl::smem_optin<uuvtc::k_policy_tc>((int)uuvtc::smem_bytes(36));
         const unsigned grid = (unsigned)((a->num_envs + uuvtc::M - 1) / uuvtc::M);
-        uuvtc::k_policy_tc<<<grid, uuvtc::NT, smem, st>>>(*a);
-        return cudaGetLastError() == cudaSuccess ? 0 : 4;
+        const cudaError_t e = uuvrl::launch_k(uuvtc::k_policy_tc, grid, uuvtc::NT, smem, st,
+                                              (a->flags & 8) != 0, *a);
+        return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 4;
     }
     const cudaError_t e = a->obs_dim <= 12 ? uuvrl::launch_policy<12>(*a, st)
                                            : uuvrl::launch_policy<36>(*a, st);
@@ -813,8 +911,10 @@ int32_t uuvsim_rl_post(const UuvRlPostArgs* a, uint64_t stream) {
         !a->norm_mean || !a->norm_var || !a->norm_count)))
         return 3;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, (a->num_envs + 1023) / 1024);
-    uuvrl::k_rl_post<<<grid, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
-    return cudaGetLastError() == cudaSuccess ? 0 : 4;
+    const cudaError_t e = uuvrl::launch_k(uuvrl::k_rl_post, grid, 1024, 0,
+                                          reinterpret_cast<cudaStream_t>(stream),
+                                          (a->flags & 1) != 0, *a);
+    return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 }  // extern "C"

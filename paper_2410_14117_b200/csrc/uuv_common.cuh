@@ -182,7 +182,8 @@ template <class T> struct EngineP {
     int32_t io_f64;        // actions / obs / reward are f64 (host ABI path), else T
     int32_t stage_obs;     // observation rows staged in shared memory, stored coalesced
     int32_t persist_blocks;   // >0: TMA-pipelined persistent paired kernel with this grid
-    int32_t pad_pb;
+    int32_t pdl;           // launched as a programmatic dependent (griddepcontrol wait /
+                           // early trigger): overlaps launch latency inside graphs
     // device buffers
     V4<T>* s0; V4<T>* s1; V4<T>* s2;
     int32_t* step;

@@ -25,6 +25,24 @@
 namespace uuv {
 
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialisation attribute may start before its predecessor on the stream
+// finishes; griddepcontrol.wait blocks until that predecessor has completed and
+// its writes are visible.  An explicit trigger (UUV_PDL_TRIGGER, launch.h) would
+// let the NEXT kernel's CTAs launch before this one ends; measured slower, so by
+// default the trigger is implicit at completion and PDL only removes the
+// launch-after-completion gap.
+__device__ __forceinline__ void pdl_enter(bool on) {
+    if (on) {
+        if (UUV_PDL_TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+}
+// late trigger: the heavy work of this CTA is done, only its stores remain
+__device__ __forceinline__ void pdl_trigger_late(bool on) {
+    if (UUV_PDL_TRIGGER == 2 && on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // stored angles are wrapped; only a teacher-forced state can lie outside
 // [-pi, pi] -- bring it in once so every sub-step can use sincos_poly
 __device__ __forceinline__ void prewrap(float s[12]) {
@@ -476,10 +494,12 @@ __global__ void __launch_bounds__(BLOCK, is_f64<T>() ? STEP_MIN_BLOCKS_F64
 k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
+    pdl_enter(p.pdl != 0);
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     StatAcc st;
     if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
                                                      reason, st);
+    pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
         const int first = blockIdx.x * BLOCK;
         flush_obs<T>(p, obs, first, min(BLOCK, p.n_env - first));
@@ -494,6 +514,7 @@ __global__ void __launch_bounds__(BLOCK, PAIR_MIN_BLOCKS)
 k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ act,
             void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
             int8_t* __restrict__ reason) {
+    pdl_enter(p.pdl != 0);
     const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
     StatAcc st;
     const bool a0 = e0 < p.n_env, a1 = e1 < p.n_env;
@@ -507,6 +528,7 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
         if (a0) one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st);
         if (a1) one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st);
     }
+    pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
         const int first = blockIdx.x * (2 * BLOCK);
         flush_obs<float>(p, obs, first, min(2 * BLOCK, p.n_env - first));
@@ -823,6 +845,27 @@ static void allow_smem() {
     done.fetch_or(bit, std::memory_order_release);
 }
 
+// <<<>>> launch, or cudaLaunchKernelEx with programmatic stream serialisation
+template <class... KArgs, class... Args>
+static cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, bool pdl, Args... args) {
+    if (!pdl) {
+        k<<<grid, block, smem, st>>>(args...);
+        return cudaSuccess;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <class T>
 cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
                             const void* act, void* obs, void* rew, uint8_t* done,
@@ -849,7 +892,9 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
 #define UUV_P(TR, M)                                                                   \
     do {                                                                               \
         allow_smem<k_step_pair<TR, M>>();                                              \
-        k_step_pair<TR, M><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
+        const cudaError_t le = launch_k(k_step_pair<TR, M>, grid, dim3(BLOCK), smem, st, \
+                                        p.pdl != 0, p, act, obs, rew, done, reason);    \
+        if (le != cudaSuccess) return le;                                              \
     } while (0)
             if (track) { if (mix) UUV_P(true, true); else UUV_P(true, false); }
             else { if (mix) UUV_P(false, true); else UUV_P(false, false); }
@@ -862,7 +907,9 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
 #define UUV_L(TR, D, M, PAT)                                                                 \
     do {                                                                                     \
         allow_smem<k_step<T, TR, D, M, PAT>>();                                              \
-        k_step<T, TR, D, M, PAT><<<grid, BLOCK, smem, st>>>(p, act, obs, rew, done, reason); \
+        const cudaError_t le = launch_k(k_step<T, TR, D, M, PAT>, grid, dim3(BLOCK), smem, st, \
+                                        p.pdl != 0, p, act, obs, rew, done, reason);          \
+        if (le != cudaSuccess) return le;                                                    \
     } while (0)
 #define UUV_LP(TR, D, M) \
     if (fossen) UUV_L(TR, D, M, PatFossen); else UUV_L(TR, D, M, PatDense)

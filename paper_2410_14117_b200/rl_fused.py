@@ -37,10 +37,11 @@ class PostArgs(ctypes.Structure):
     _fields_ = [("num_envs", ctypes.c_uint64), ("obs_dim", ctypes.c_uint32),
                 ("n_part", ctypes.c_uint32), ("stats_part", _f), ("norm_mean", _f),
                 ("norm_var", _f), ("norm_count", _f), ("rew_in", _f), ("done_in", _f),
-                ("rew_out", _f), ("done_out", _f), ("noise_ctr", _f)]
+                ("rew_out", _f), ("done_out", _f), ("noise_ctr", _f),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
-SAMPLE, NORM_STATS, VALUE_ONLY = 1, 2, 4
+SAMPLE, NORM_STATS, VALUE_ONLY, PDL = 1, 2, 4, 8
 
 
 def _p(t):
@@ -49,8 +50,11 @@ def _p(t):
 
 class FusedActorCritic:
     def __init__(self, policy, norm, num_envs: int, seed: int = 0, env_offset: int = 0,
-                 tensor_cores: bool = True):
+                 tensor_cores: bool = True, pdl: bool = False):
         self.lib = _core.load()
+        # programmatic dependent launch of the policy / post kernels (tensor-core
+        # path): their CTAs start while the previous kernel of the step finishes
+        self.pdl = bool(pdl) and tensor_cores
         self.policy, self.norm = policy, norm
         self.M = int(num_envs)
         self.D = policy.a1.weight.shape[1]
@@ -96,7 +100,7 @@ class FusedActorCritic:
     def act(self, obs, nobs=None, raw=None, act=None, logp=None, value=None,
             sample: bool = True, update_norm: bool = True, value_only: bool = False):
         flags = (SAMPLE if sample else 0) | (NORM_STATS if update_norm else 0) | \
-                (VALUE_ONLY if value_only else 0)
+                (VALUE_ONLY if value_only else 0) | (PDL if self.pdl else 0)
         a = self._args(obs, flags, nobs, raw, act, logp, value)
         _core.check(self.lib, self.lib.uuvsim_rl_policy_act(
             ctypes.byref(a), torch.cuda.current_stream().cuda_stream))
@@ -105,7 +109,7 @@ class FusedActorCritic:
         nm = self.norm
         a = PostArgs(self.M, self.D, self.n_part if update_norm else 0, _p(self.stats_part),
                      _p(nm.mean), _p(nm.var), _p(nm.count), _p(rew), _p(done), _p(rew_out),
-                     _p(done_out), _p(self.noise_ctr))
+                     _p(done_out), _p(self.noise_ctr), 1 if self.pdl else 0, 0)
         _core.check(self.lib, self.lib.uuvsim_rl_post(
             ctypes.byref(a), torch.cuda.current_stream().cuda_stream))
 

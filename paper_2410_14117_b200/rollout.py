@@ -142,7 +142,7 @@ class Rollout:
     """Horizon buffers + the graph-captured collection loop for one env slab."""
 
     def __init__(self, env, policy: ActorCritic, norm: RunningNorm, cfg: TrainConfig,
-                 use_graph: bool = True, fused: bool | None = None):
+                 use_graph: bool = True, fused: bool | None = None, pdl: bool = True):
         self.env, self.policy, self.norm, self.cfg = env, policy, norm, cfg
         dev = torch.device("cuda", env.device_index)
         T, M = cfg.horizon, env.num_envs
@@ -165,8 +165,10 @@ class Rollout:
         self.fused = None
         if fused:
             from .rl_fused import FusedActorCritic
+            # pdl: policy / step / post launched as programmatic dependents, so
+            # each kernel's CTAs are resident before its predecessor finishes
             self.fused = FusedActorCritic(policy, norm, M, seed=cfg.seed + 7,
-                                          env_offset=getattr(env, "env_offset", 0))
+                                          env_offset=getattr(env, "env_offset", 0), pdl=pdl)
         self.env_obs = None
 
     def reset(self, seed: int):
@@ -201,12 +203,19 @@ class Rollout:
         F, env = self.fused, self.env
         obs = self.env_obs
         F.prepare()   # parameters changed since the last horizon (PPO update)
-        for t in range(self.cfg.horizon):
-            F.act(obs, nobs=self.obs_buf[t], raw=self.act_buf[t], act=self.act_in,
-                  logp=self.logp_buf[t], value=self.val_buf[t])
-            obs, r, d, _ = env.step_tensors(self.act_in)
-            F.post(r, d, self.rew_buf[t], self.done_buf[t])
-        F.act(obs, value=self.boot_value, sample=False, update_norm=False, value_only=True)
+        pdl = F.pdl and hasattr(env, "set_pdl")
+        if pdl:
+            env.set_pdl(True)
+        try:
+            for t in range(self.cfg.horizon):
+                F.act(obs, nobs=self.obs_buf[t], raw=self.act_buf[t], act=self.act_in,
+                      logp=self.logp_buf[t], value=self.val_buf[t])
+                obs, r, d, _ = env.step_tensors(self.act_in)
+                F.post(r, d, self.rew_buf[t], self.done_buf[t])
+            F.act(obs, value=self.boot_value, sample=False, update_norm=False, value_only=True)
+        finally:
+            if pdl:
+                env.set_pdl(False)
         self.env_obs = obs
 
     def collect(self):

@@ -268,6 +268,48 @@ def test_torch_cuda_graph_capture():
     assert np.array_equal(a.states(), b.states())
 
 
+@pytest.mark.parametrize("n,pair", [(4096, "off"), (300000, "on")])
+def test_programmatic_launch_step_is_bit_identical(n, pair):
+    """uuvsim_dev_set_pdl: the step launched as a programmatic dependent of a
+    torch kernel that writes its actions (eager and in a torch CUDA graph) gives
+    the same states, outputs and counters as plain stream order."""
+    cfg = _cfg(kind="circle", n=n, episode_len=30)
+    cfg["device"]["pair"] = pair
+    a, b = uuv.B200EnvBatch(cfg), uuv.B200EnvBatch(cfg)
+    a.set_pdl(True)
+    base = a.bench_actions_tensor()
+    act_a, act_b = torch.empty_like(base), torch.empty_like(base)
+
+    def step(env, act, k):
+        torch.mul(base, 0.5 + 0.01 * k, out=act)   # the predecessor writes the actions
+        return env.step_tensors(act)
+
+    for k in range(40):
+        oa, ra, da, _ = step(a, act_a, k)
+        ob, rb, db, _ = step(b, act_b, k)
+        assert torch.equal(oa, ob) and torch.equal(ra, rb) and torch.equal(da, db)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(a, act_a, 0)
+        step(b, act_b, 0)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k in range(5):
+            step(a, act_a, k)
+    for _ in range(8):
+        g.replay()
+        for k in range(5):
+            step(b, act_b, k)
+    torch.cuda.synchronize()
+    assert np.array_equal(a.states(), b.states())
+    assert np.array_equal(a.step_counts(), b.step_counts())
+    assert np.array_equal(np.stack(a.counters()), np.stack(b.counters()))
+    a.close()
+    b.close()
+
+
 def test_sharding_invariance_on_device():
     whole_cfg = _cfg(kind="helix", dr="episode", episode_len=50, n=6000, seed=4)
     halves = [_cfg(kind="helix", dr="episode", episode_len=50, n=3000, seed=4, env_offset=o)

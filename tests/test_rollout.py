@@ -232,6 +232,34 @@ def test_fused_collect_matches_framework_collect():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("use_graph", [False, True], ids=["eager", "graph"])
+def test_programmatic_launch_is_bit_identical(use_graph):
+    """The fused rollout with programmatic dependent launches (policy / step /
+    post waiting in griddepcontrol instead of stream order) produces exactly the
+    buffers of the plain launches: sampled actions, rewards, terminations,
+    normaliser statistics."""
+    make = _make_env("circle", dr=True)
+    cfg = R.TrainConfig(num_envs=3000, horizon=24)
+    outs = []
+    for pdl in (False, True):
+        env = make(cfg.num_envs, 5)
+        pol = _random_policy(env.obs_dim, env.action_dim, 4)
+        norm = R.RunningNorm(env.obs_dim, "cuda")
+        ro = R.Rollout(env, pol, norm, cfg, use_graph=use_graph, fused=True, pdl=pdl)
+        assert ro.fused.pdl == pdl
+        ro.reset(5)
+        ro.collect()
+        ro.collect()        # graph: warm-up + capture + replay, then a second replay
+        torch.cuda.synchronize()
+        outs.append([b.clone() for b in (ro.obs_buf, ro.act_buf, ro.logp_buf, ro.rew_buf,
+                                         ro.done_buf, ro.val_buf, ro.boot_value, norm.mean,
+                                         norm.var, norm.count, ro.fused.noise_ctr)])
+        env.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
 def test_gae_fused_matches_reference():
     g = torch.Generator(device="cuda").manual_seed(2)
     T, M = 37, 1000

@@ -19,13 +19,14 @@ def main():
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--horizon", type=int, default=64)
+    ap.add_argument("--no-pdl", action="store_true")
     a = ap.parse_args()
     env = uuv.batch_create(uuv.TaskSpec(kind="circle"), uuv.bluerov2_params(), None, 16384, 0,
                            device=0)
     cfg = R.TrainConfig(num_envs=16384, horizon=a.horizon)
     pol = R.ActorCritic(env.obs_dim, env.action_dim).cuda()
     ro = R.Rollout(env, pol, R.RunningNorm(env.obs_dim, "cuda"), cfg, use_graph=not a.eager,
-                   fused=not a.unfused)
+                   fused=not a.unfused, pdl=not a.no_pdl)
     ro.reset(0)
     ro.collect()
     torch.cuda.synchronize()
