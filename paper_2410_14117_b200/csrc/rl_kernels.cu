@@ -417,6 +417,24 @@ __host__ __device__ inline uint32_t cm_off(int row, int k, int KC) {
     return (uint32_t)((((row >> 3) * KC + (k >> 2)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
 }
 
+#ifndef UUV_TC_FAST_TANH
+#define UUV_TC_FAST_TANH 1
+#endif
+// epilogue tanh: (e^2x - 1) / (e^2x + 1) from one MUFU.EX2 and one MUFU.RCP on a
+// clamped argument (|err| < 4e-7 absolute; t - 1 is exact for t in [1/2, 2], so
+// small |x| keeps its accuracy), or libdevice tanhf
+__device__ __forceinline__ float tanh_epi(float x) {
+#if UUV_TC_FAST_TANH
+    x = fminf(fmaxf(x, -9.0f), 9.0f);
+    float t, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(x * 2.88539008177792681f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t + 1.0f));
+    return (t - 1.0f) * r;
+#else
+    return tanhf(x);
+#endif
+}
+
 __device__ __forceinline__ float tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -523,7 +541,7 @@ __device__ __forceinline__ void epi_hidden(uint32_t tacc, const float* b, unsign
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int j = 16 * c16 + 4 * q + t;
-                const float x = tanhf(v[4 * q + t] + b[j]);
+                const float x = tanh_epi(v[4 * q + t] + b[j]);
                 hp[t] = tf32(x);
                 lp[t] = tf32(x - hp[t]);
             }
@@ -534,20 +552,26 @@ __device__ __forceinline__ void epi_hidden(uint32_t tacc, const float* b, unsign
     }
 }
 
-// one layer: D(tmem) = A B^T with 3xTF32, K = kdim; commit to bar
+// one layer: D(tmem) = A B^T with 3xTF32, K = kdim; commit to bar.  The four
+// descriptors are built once; stepping K by 8 (two core matrices, 256 B) adds 16
+// to the start-address field (address >> 4; shared addresses stay < 256 KB)
 __device__ __forceinline__ void issue_layer(uint32_t tmem, const unsigned char* a_hi,
                                             const unsigned char* a_lo, const unsigned char* b_hi,
-                                            const unsigned char* b_lo, int kdim, uint64_t* bar) {
+                                            const unsigned char* b_lo, int kdim,
+                                            uint64_t* bar /* NULL: no commit */) {
     const int KC = kdim / 4;
-    const uint32_t ah = s_u32(a_hi), al = s_u32(a_lo), bh = s_u32(b_hi), bl = s_u32(b_lo);
+    const uint64_t dah = umma_desc(s_u32(a_hi), KC), dal = umma_desc(s_u32(a_lo), KC);
+    const uint64_t dbh = umma_desc(s_u32(b_hi), KC), dbl = umma_desc(s_u32(b_lo), KC);
+#pragma unroll 1
     for (int ks = 0; ks < kdim / 8; ++ks) {   // K = 8 per MMA: two core matrices along K
-        const uint32_t off = ks * 256u;
-        mma_tf32(tmem, umma_desc(ah + off, KC), umma_desc(bh + off, KC), ks > 0 ? 1u : 0u);
-        mma_tf32(tmem, umma_desc(ah + off, KC), umma_desc(bl + off, KC), 1u);
-        mma_tf32(tmem, umma_desc(al + off, KC), umma_desc(bh + off, KC), 1u);
+        const uint64_t off = (uint64_t)ks * 16u;
+        mma_tf32(tmem, dah + off, dbh + off, ks > 0 ? 1u : 0u);
+        mma_tf32(tmem, dah + off, dbl + off, 1u);
+        mma_tf32(tmem, dal + off, dbh + off, 1u);
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 ::"r"(s_u32(bar)) : "memory");
+    if (bar)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(s_u32(bar)) : "memory");
 }
 
 constexpr int NT = 2 * M;   // threads: two per env (TMEM lane quarter = warp % 4, column half = warp / 4)
@@ -579,8 +603,8 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {   // 64 TMEM columns: one fp32 128 x 64 accumulator
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;"
+    if (warp == 0) {   // 128 TMEM columns: two fp32 128 x 64 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;"
                      ::"r"(s_u32(&tmem_base_sh)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -608,14 +632,15 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     const uint64_t e = (uint64_t)blockIdx.x * M + row;
     const bool active = e < a.num_envs;
     const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;   // issued early: one round trip
-    float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][37] (A_h unused yet)
+    float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][D] (A_h unused yet)
     const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
     const int nvalid = left < (uint64_t)M ? (int)left : M;
-    {   // the CTA's rows are one contiguous span: coalesced 16-byte loads by every
-        // thread, all issued before any shared-memory store (one memory round trip)
+    {   // the CTA's rows are one contiguous span in global AND shared memory: a
+        // straight coalesced copy, every 16-byte load issued before any store
         const float* src = a.obs + (uint64_t)blockIdx.x * M * D;
         const int nf = nvalid * D;
         constexpr int PER = (M * 36 / 4 + NT - 1) / NT;   // float4 per thread at D = 36
+        int done_f = 0;
         if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
             const int n4 = nf >> 2;
             float4 buf[PER];
@@ -627,29 +652,12 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 const int i = tid + j * NT;
-                if (i < n4) {
-                    const float* bv = &buf[j].x;
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int f = 4 * i + t, r = f / D;
-                        raw[r * 37 + (f - r * D)] = bv[t];
-                    }
-                }
+                if (i < n4) reinterpret_cast<float4*>(raw)[i] = buf[j];
             }
-            for (int f = (n4 << 2) + tid; f < nf; f += NT) {
-                const int r = f / D;
-                raw[r * 37 + (f - r * D)] = __ldg(src + f);
-            }
-        } else {
-            for (int f = tid; f < nf; f += NT) {
-                const int r = f / D;
-                raw[r * 37 + (f - r * D)] = __ldg(src + f);
-            }
+            done_f = n4 << 2;
         }
-        for (int f = nf + tid; f < M * D; f += NT) {   // rows past the last env
-            const int r = f / D;
-            raw[r * 37 + (f - r * D)] = 0.0f;
-        }
+        for (int f = done_f + tid; f < nf; f += NT) raw[f] = __ldg(src + f);
+        for (int f = nf + tid; f < M * D; f += NT) raw[f] = 0.0f;   // rows past the last env
     }
     __syncthreads();
     if ((a.flags & 2) && tid < 2 * D) {
@@ -661,12 +669,12 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         for (; r + 4 <= nvalid; r += 4) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const double v = raw[(r + q) * 37 + d];
+                const double v = raw[(r + q) * D + d];
                 acc4[q] += tid < D ? v : v * v;
             }
         }
         for (; r < nvalid; ++r) {
-            const double v = raw[r * 37 + d];
+            const double v = raw[r * D + d];
             acc4[0] += tid < D ? v : v * v;
         }
         const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
@@ -674,7 +682,9 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         a.stats_part[(size_t)row2 * 2 * D + tid] = acc;
         a.stats_part[(size_t)(row2 + 1) * 2 * D + tid] = 0.0;   // FFMA-kernel granularity
     }
-    // normalise: the two column halves split the K chunks
+    // normalise: the two column halves split the K chunks; the fp32 rows are staged
+    // in A_h's lo half (unused yet) and stored to nobs_out coalesced afterwards
+    float* zst = reinterpret_cast<float*>(ah_lo);
 #pragma unroll 1
     for (int k4 = ch; 4 * k4 < K1; k4 += 2) {
         float4 hi, lo;
@@ -685,10 +695,10 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
             const int k = 4 * k4 + t;
             float zk = 0.0f;
             if (k < D) {   // RunningNorm.normalize in fp64
-                double v = ((double)raw[row * 37 + k] - nsc[k]) * nsc[36 + k];
+                double v = ((double)raw[row * D + k] - nsc[k]) * nsc[36 + k];
                 v = fmin(fmax(v, -a.norm_clip), a.norm_clip);
                 zk = (float)v;
-                if (active && a.nobs_out) a.nobs_out[e * D + k] = zk;
+                zst[row * D + k] = zk;
             }
             hp[t] = tf32(zk);
             lp[t] = tf32(zk - hp[t]);
@@ -700,24 +710,46 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // A_z -> tensor-core proxy
     __syncthreads();
     mbar_wait(&bars[0], 0);                                        // weights landed
-    const uint32_t tacc = tmem + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lanes
-
-    // ---- critic: value = cv . tanh(W2c tanh(W1c z + b1c) + b2c) + cvb
-    if (tid == 0) {
+    if (tid == 0) {   // round 1: critic layer 1 (runs while the normalised rows go out)
         tc_fence_after();
         issue_layer(tmem, az_hi, az_lo, wimg + g.w1c_hi, wimg + g.w1c_lo, K1, &bars[1]);
     }
+    if (a.nobs_out) {   // the CTA's normalised rows: one contiguous span
+        float* dst = a.nobs_out + (uint64_t)blockIdx.x * M * D;
+        const int nf = nvalid * D;
+        int done_f = 0;
+        if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            const int n4 = nf >> 2;
+            for (int i = tid; i < n4; i += NT)
+                reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(zst)[i];
+            done_f = n4 << 2;
+        }
+        for (int f = done_f + tid; f < nf; f += NT) dst[f] = zst[f];
+    }
+    __syncthreads();   // staging read out before the first epilogue overwrites A_h
+    // two fp32 128 x 64 accumulators: acc0 (columns 0-63), acc1 (64-127)
+    const uint32_t tacc = tmem + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lanes
+    const uint32_t tacc1 = tacc + (uint32_t)H;
+
+    // critic: value = cv . tanh(W2c tanh(W1c z + b1c) + b2c) + cvb
+    // actor:  mean = tanh(am tanh(W2a tanh(W1a z + b1a) + b2a) + amb)
+    // The chains are independent: the actor's first layer (A_z -> acc1) is issued
+    // together with the critic's second (A_h -> acc0), so three MMA rounds and
+    // three epilogue phases instead of four of each.
     mbar_wait(&bars[1], 0);
     tc_fence_after();
     epi_hidden(tacc, sp + S_B1C, ah_hi, ah_lo, row, ch);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {   // round 2: critic layer 2 (acc0) + actor layer 1 (acc1), one commit
         tc_fence_after();
+        if (!value_only)
+            issue_layer(tmem + (uint32_t)H, az_hi, az_lo, wimg + g.w1a_hi, wimg + g.w1a_lo, K1,
+                        nullptr);
         issue_layer(tmem, ah_hi, ah_lo, wimg + g.w2c_hi, wimg + g.w2c_lo, H, &bars[1]);
     }
-    mbar_wait(&bars[1], 1);
+    mbar_wait(&bars[1], 1);   // both done: A_h is free again
     tc_fence_after();
     {
         float vp = 0.0f;
@@ -727,33 +759,24 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
             tmem_ld16(tacc + 16 * c16, v);
 #pragma unroll
             for (int t = 0; t < 16; ++t)
-                vp = fmaf(sp[S_CV + 16 * c16 + t], tanhf(v[t] + sp[S_B2C + 16 * c16 + t]), vp);
+                vp = fmaf(sp[S_CV + 16 * c16 + t], tanh_epi(v[t] + sp[S_B2C + 16 * c16 + t]), vp);
         }
         red[ch][row] = vp;
     }
-    // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
-    // the mean head; A_z's region is free once the actor's first layer has consumed it
-    float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;   // (after actor L2 only)
+    if (!value_only) epi_hidden(tacc1, sp + S_B1A, ah_hi, ah_lo, row, ch);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
-    __syncthreads();   // all TMEM reads of the critic done; red complete
+    __syncthreads();   // red complete; actor A_h complete
     const float value = red[0][row] + red[1][row] + sp[S_CVB];
+    // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
+    // the mean head, over A_h once the actor's second layer has consumed it
+    float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;
     if (!value_only) {
-        // ---- actor: mean = tanh(am tanh(W2a tanh(W1a z + b1a) + b2a) + amb)
-        if (tid == 0) {
-            tc_fence_after();
-            issue_layer(tmem, az_hi, az_lo, wimg + g.w1a_hi, wimg + g.w1a_lo, K1, &bars[1]);
-        }
-        mbar_wait(&bars[1], 0);
-        tc_fence_after();
-        epi_hidden(tacc, sp + S_B1A, ah_hi, ah_lo, row, ch);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
+        if (tid == 0) {   // round 3: actor layer 2
             tc_fence_after();
             issue_layer(tmem, ah_hi, ah_lo, wimg + g.w2a_hi, wimg + g.w2a_lo, H, &bars[1]);
         }
-        mbar_wait(&bars[1], 1);   // A_h consumed: hrow may overwrite it
+        mbar_wait(&bars[1], 0);   // A_h consumed: hrow may overwrite it
         tc_fence_after();
 #pragma unroll 1
         for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
@@ -762,16 +785,17 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
 #pragma unroll
             for (int t = 0; t < 16; t += 4)
                 *reinterpret_cast<float4*>(hrow + 16 * c16 + t) = make_float4(
-                    tanhf(v[t] + sp[S_B2A + 16 * c16 + t]), tanhf(v[t + 1] + sp[S_B2A + 16 * c16 + t + 1]),
-                    tanhf(v[t + 2] + sp[S_B2A + 16 * c16 + t + 2]),
-                    tanhf(v[t + 3] + sp[S_B2A + 16 * c16 + t + 3]));
+                    tanh_epi(v[t] + sp[S_B2A + 16 * c16 + t]),
+                    tanh_epi(v[t + 1] + sp[S_B2A + 16 * c16 + t + 1]),
+                    tanh_epi(v[t + 2] + sp[S_B2A + 16 * c16 + t + 2]),
+                    tanh_epi(v[t + 3] + sp[S_B2A + 16 * c16 + t + 3]));
         }
     }
     tc_fence_before();
     __syncthreads();
     if (UUV_PDL_TRIGGER == 2 && pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
     if (value_only) {
         if (active && ch == 0 && a.value_out) a.value_out[e] = value;
         return;
