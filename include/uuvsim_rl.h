@@ -64,7 +64,9 @@ typedef struct {
 typedef struct {
     uint64_t num_envs;
     uint32_t obs_dim;
-    uint32_t n_part;         /* number of partial rows written by the policy launch */
+    uint32_t n_part;         /* number of partial rows written by the policy launch:
+                                ceil(M / 128) for the tensor-core kernel (one per CTA),
+                                uuvsim_rl_policy_blocks(M) for the CUDA-core kernel */
     const double* stats_part;
     double* norm_mean;       /* [D] updated in place */
     double* norm_var;        /* [D] */
@@ -78,7 +80,8 @@ typedef struct {
     uint32_t reserved;
 } UuvRlPostArgs;
 
-/* partial rows the policy launch writes for num_envs (size of stats_part / (2 D)) */
+/* partial rows the stats_part buffer must hold for num_envs (size / (2 D)); the
+ * tensor-core kernel writes the first ceil(num_envs / 128) of them */
 uint32_t uuvsim_rl_policy_blocks(uint64_t num_envs);
 /* bytes of the tensor-core weight image for obs_dim (multiple of 16) */
 uint64_t uuvsim_rl_image_bytes(uint32_t obs_dim);

@@ -264,12 +264,16 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
         if (UUV_PDL_TRIGGER >= 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         asm volatile("griddepcontrol.wait;" ::: "memory");
     }
-    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < a.num_envs) {
-        if (a.rew_in && a.rew_out) a.rew_out[e] = a.rew_in[e];
-        if (a.done_in && a.done_out) a.done_out[e] = a.done_in[e] ? 1.0f : 0.0f;
+    if (blockIdx.x != 0) {   // blocks 1.. copy reward / done; block 0 merges the statistics
+        const uint64_t e = (uint64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x;
+        if (e < a.num_envs) {
+            const float r = a.rew_in && a.rew_out ? a.rew_in[e] : 0.0f;
+            const uint8_t d = a.done_in && a.done_out ? a.done_in[e] : 0;
+            if (a.rew_in && a.rew_out) a.rew_out[e] = r;
+            if (a.done_in && a.done_out) a.done_out[e] = d ? 1.0f : 0.0f;
+        }
+        return;
     }
-    if (blockIdx.x != 0) return;
     __shared__ double tot_sh;
     __shared__ double sums[2 * 36];
     const int D = (int)a.obs_dim;
@@ -280,28 +284,34 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
         const double cnt = *a.norm_count;
         const double m = owner ? a.norm_mean[threadIdx.x] : 0.0;
         const double v = owner ? a.norm_var[threadIdx.x] : 0.0;
-        // one warp per (sum, dim) column (2 D <= 72 columns: at most 3 per warp of
-        // a 1024-thread block): lanes stride the partial rows, every load of all of
-        // the warp's columns in flight together, then a fixed shuffle tree --
-        // deterministic
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        constexpr int CPW = 3;
-        double acc[CPW] = {0.0, 0.0, 0.0};
-#pragma unroll 8
-        for (uint32_t b = lane; b < a.n_part; b += 32) {
+        // the partial rows are row-major [n_part][2 D]: thread (g, c) sums column c
+        // over rows g, g + G, g + 2 G, ... (G = blockDim / 2 D groups) -- each
+        // row read by consecutive threads (coalesced), every load of a batch in
+        // flight before the adds -- then the G group sums of a column are added
+        // in group order (fixed order: deterministic)
+        __shared__ double gsum[1024];
+        const int ncol = 2 * D, ngrp = (int)blockDim.x / ncol;
+        const int g = (int)threadIdx.x / ncol, c = (int)threadIdx.x - g * ncol;
+        if (g < ngrp) {
+            constexpr int RPT = 8;
+            double part = 0.0;
+            for (uint32_t r0 = (uint32_t)g; r0 < a.n_part; r0 += (uint32_t)(RPT * ngrp)) {
+                double x[RPT];
 #pragma unroll
-            for (int c = 0; c < CPW; ++c) {
-                const int col = warp + c * nw;
-                if (col < 2 * D) acc[c] += a.stats_part[(size_t)b * 2 * D + col];
+                for (int j = 0; j < RPT; ++j) {
+                    const uint32_t r = r0 + (uint32_t)(j * ngrp);
+                    x[j] = r < a.n_part ? a.stats_part[(size_t)r * ncol + c] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) part += x[j];
             }
+            gsum[threadIdx.x] = part;
         }
-#pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-            double x = acc[c];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            const int col = warp + c * nw;
-            if (lane == 0 && col < 2 * D) sums[col] = x;
+        __syncthreads();
+        if ((int)threadIdx.x < ncol) {
+            double t = 0.0;
+            for (int q = 0; q < ngrp; ++q) t += gsum[q * ncol + threadIdx.x];
+            sums[threadIdx.x] = t;
         }
         __syncthreads();
         const double tot = cnt + n;
@@ -678,9 +688,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
             acc4[0] += tid < D ? v : v * v;
         }
         const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-        const uint32_t row2 = 2u * blockIdx.x;
-        a.stats_part[(size_t)row2 * 2 * D + tid] = acc;
-        a.stats_part[(size_t)(row2 + 1) * 2 * D + tid] = 0.0;   // FFMA-kernel granularity
+        a.stats_part[(size_t)blockIdx.x * 2 * D + tid] = acc;   // one row per CTA
     }
     // normalise: the two column halves split the K chunks; the fp32 rows are staged
     // in A_h's lo half (unused yet) and stored to nobs_out coalesced afterwards
@@ -892,7 +900,8 @@ int32_t uuvsim_rl_gae(const float* rew, const float* val, const float* done, con
 }
 
 uint32_t uuvsim_rl_policy_blocks(uint64_t num_envs) {
-    // rows for both kernels: 64-env FFMA blocks, or two rows per 128-env tensor-core CTA
+    // buffer rows: one per 64-env CUDA-core block (the tensor-core kernel writes one
+    // per 128-env CTA, the first half)
     return (uint32_t)(2 * ((num_envs + uuvtc::M - 1) / uuvtc::M));
 }
 
@@ -934,7 +943,7 @@ int32_t uuvsim_rl_post(const UuvRlPostArgs* a, uint64_t stream) {
     if (!a || a->num_envs == 0 || a->obs_dim > 36 || (a->n_part && (!a->stats_part ||
         !a->norm_mean || !a->norm_var || !a->norm_count)))
         return 3;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, (a->num_envs + 1023) / 1024);
+    const unsigned grid = (unsigned)(1 + (a->num_envs + 1023) / 1024);   // + statistics block
     const cudaError_t e = uuvrl::launch_k(uuvrl::k_rl_post, grid, 1024, 0,
                                           reinterpret_cast<cudaStream_t>(stream),
                                           (a->flags & 1) != 0, *a);

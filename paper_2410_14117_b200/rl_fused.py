@@ -68,8 +68,11 @@ class FusedActorCritic:
         dev = policy.a1.weight.device
         self.seed, self.env_offset = int(seed), int(env_offset)
         self.noise_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.n_part = int(self.lib.uuvsim_rl_policy_blocks(self.M))
-        self.stats_part = torch.zeros(self.n_part * 2 * self.D, dtype=torch.float64, device=dev)
+        rows = int(self.lib.uuvsim_rl_policy_blocks(self.M))
+        self.stats_part = torch.zeros(rows * 2 * self.D, dtype=torch.float64, device=dev)
+        # rows the policy launch writes: one per 128-env CTA on the tensor cores,
+        # one per 64-env block on the CUDA cores
+        self.n_part = (self.M + 127) // 128 if tensor_cores else rows
         # tcgen05 path: weights split to 3xTF32 in the UMMA layout by prepare()
         self.image = None
         if tensor_cores:
