@@ -535,12 +535,18 @@ __global__ void k_rl_prepare(const UuvRlPolicyArgs a, unsigned char* img) {
     }
 }
 
-// epilogue of a hidden layer for 32 of this env's units (column half ch):
+#ifndef UUV_TC_NQ
+#define UUV_TC_NQ 4   // threads per env (column groups); 8 or 16 warps per CTA
+#endif
+constexpr int NQ = UUV_TC_NQ;           // column groups per env: 2 or 4
+constexpr int CPQ = 4 / NQ;             // 16-column accumulator chunks per thread
+
+// epilogue of a hidden layer for 64 / NQ of this env's units (column group ch):
 // tanh(acc + b) -> next layer's A operand (hi/lo)
 __device__ __forceinline__ void epi_hidden(uint32_t tacc, const float* b, unsigned char* a_hi,
                                            unsigned char* a_lo, int row, int ch) {
 #pragma unroll 1   // compact code: the CTA's warps run in near lockstep, an icache miss stalls all
-    for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+    for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
         float v[16];
         tmem_ld16(tacc + 16 * c16, v);
 #pragma unroll
@@ -584,14 +590,14 @@ __device__ __forceinline__ void issue_layer(uint32_t tmem, const unsigned char* 
                      ::"r"(s_u32(bar)) : "memory");
 }
 
-constexpr int NT = 2 * M;   // threads: two per env (TMEM lane quarter = warp % 4, column half = warp / 4)
+constexpr int NT = NQ * M;   // threads: NQ per env (TMEM lane quarter = warp % 4, column group = warp / 4)
 
 __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[2];   // [0] weights landed, [1] MMA done
     __shared__ uint32_t tmem_base_sh;
     __shared__ double nsc[2 * 36];              // normaliser mean, 1 / sqrt(var + 1e-8)
-    __shared__ float red[2][M];                 // cross-half partials
+    __shared__ float red[NQ][M];                // cross-group partials
     const int D = (int)a.obs_dim, A = (int)a.act_dim;
     const bool value_only = (a.flags & 4) != 0;
     const Img g = img_layout(D);
@@ -604,7 +610,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     const float* sp = reinterpret_cast<const float*>(wimg + g.small);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int row = ((warp & 3) << 5) + lane;            // env in CTA = TMEM lane
-    const int ch = warp >> 2;                            // column half
+    const int ch = warp >> 2;                            // column group
     const bool pdl = (a.flags & 8) != 0;                 // programmatic dependent launch
     if (pdl && UUV_PDL_TRIGGER == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -694,7 +700,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     // in A_h's lo half (unused yet) and stored to nobs_out coalesced afterwards
     float* zst = reinterpret_cast<float*>(ah_lo);
 #pragma unroll 1
-    for (int k4 = ch; 4 * k4 < K1; k4 += 2) {
+    for (int k4 = ch; 4 * k4 < K1; k4 += NQ) {
         float4 hi, lo;
         float* hp = &hi.x;
         float* lp = &lo.x;
@@ -762,7 +768,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     {
         float vp = 0.0f;
 #pragma unroll 1
-        for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+        for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
             float v[16];
             tmem_ld16(tacc + 16 * c16, v);
 #pragma unroll
@@ -775,7 +781,8 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();   // red complete; actor A_h complete
-    const float value = red[0][row] + red[1][row] + sp[S_CVB];
+    const float value = (NQ == 4 ? (red[0][row] + red[1][row]) + (red[NQ - 2][row] + red[NQ - 1][row])
+                                 : red[0][row] + red[1][row]) + sp[S_CVB];
     // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
     // the mean head, over A_h once the actor's second layer has consumed it
     float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;
@@ -787,7 +794,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         mbar_wait(&bars[1], 0);   // A_h consumed: hrow may overwrite it
         tc_fence_after();
 #pragma unroll 1
-        for (int c16 = 2 * ch; c16 < 2 * ch + 2; ++c16) {
+        for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
             float v[16];
             tmem_ld16(tacc + 16 * c16, v);
 #pragma unroll
@@ -808,11 +815,11 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         if (active && ch == 0 && a.value_out) a.value_out[e] = value;
         return;
     }
-    // action dims: half ch takes Box-Muller pairs 2 ch and 2 ch + 1 (dims 4 ch .. 4 ch + 3)
+    // action dims: group ch takes Box-Muller pairs CPQ ch .. CPQ ch + CPQ - 1 (two dims each)
     const uint64_t gid = a.env_offset + e;
     float logp = 0.0f;
 #pragma unroll 1
-    for (int p = 2 * ch; p < 2 * ch + 2; ++p) {
+    for (int p = CPQ * ch; p < CPQ * ch + CPQ; ++p) {
         if (2 * p >= A) break;
         float eps0 = 0.0f, eps1 = 0.0f;
         if (a.flags & 1) {   // Box-Muller on the counter-based stream
@@ -852,7 +859,9 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     red[ch][row] = logp;
     __syncthreads();
     if (active && ch == 0) {
-        if (a.logp_out) a.logp_out[e] = red[0][row] + red[1][row];
+        if (a.logp_out)
+            a.logp_out[e] = NQ == 4 ? (red[0][row] + red[1][row]) + (red[NQ - 2][row] + red[NQ - 1][row])
+                                    : red[0][row] + red[1][row];
         if (a.value_out) a.value_out[e] = value;
     }
 }
