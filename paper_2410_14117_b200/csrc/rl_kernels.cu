@@ -483,6 +483,18 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+// 8 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
 // 16 consecutive fp32 accumulator columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -496,6 +508,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N> __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[N]) {
+    if constexpr (N == 16) tmem_ld16(taddr, v);
+    else tmem_ld8(taddr, v);
 }
 
 // weight image: hi/lo tf32 splits in the core-matrix layout + the small block
@@ -536,32 +552,46 @@ __global__ void k_rl_prepare(const UuvRlPolicyArgs a, unsigned char* img) {
 }
 
 #ifndef UUV_TC_NQ
-#define UUV_TC_NQ 4   // threads per env (column groups); 8 or 16 warps per CTA
+#define UUV_TC_NQ 4   // threads per env (column groups): 2 / 4 / 8 measured 24.6 / 23.1 / 23.7 us
+                      // per C4 loop step
 #endif
-constexpr int NQ = UUV_TC_NQ;           // column groups per env: 2 or 4
-constexpr int CPQ = 4 / NQ;             // 16-column accumulator chunks per thread
+constexpr int NQ = UUV_TC_NQ;           // column groups per env: 2, 4 or 8
+constexpr int CW = 64 / NQ;             // accumulator columns per thread
+constexpr int CK = CW < 16 ? CW : 16;   // columns per tcgen05.ld
+constexpr int CPQ = CW / CK;            // tcgen05.ld chunks per thread
+constexpr int PPQ = NQ < 4 ? 4 / NQ : 1;   // Box-Muller pairs per thread (4 pairs: A <= 8)
+
+// fixed-order sum of the NQ group partials of one env
+__device__ __forceinline__ float sum_groups(const float (*red)[128], int row) {
+    if constexpr (NQ == 2) return red[0][row] + red[1][row];
+    else if constexpr (NQ == 4) return (red[0][row] + red[1][row]) + (red[2][row] + red[3][row]);
+    else
+        return ((red[0][row] + red[1][row]) + (red[2][row] + red[3][row])) +
+               ((red[4][row] + red[5][row]) + (red[6][row] + red[7][row]));
+}
 
 // epilogue of a hidden layer for 64 / NQ of this env's units (column group ch):
 // tanh(acc + b) -> next layer's A operand (hi/lo)
 __device__ __forceinline__ void epi_hidden(uint32_t tacc, const float* b, unsigned char* a_hi,
                                            unsigned char* a_lo, int row, int ch) {
 #pragma unroll 1   // compact code: the CTA's warps run in near lockstep, an icache miss stalls all
-    for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
-        float v[16];
-        tmem_ld16(tacc + 16 * c16, v);
+    for (int cc = 0; cc < CPQ; ++cc) {
+        const int c0 = ch * CW + cc * CK;
+        float v[CK];
+        tmem_ld<CK>(tacc + c0, v);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < CK / 4; ++q) {
             float4 hi, lo;
             float* hp = &hi.x;
             float* lp = &lo.x;
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                const int j = 16 * c16 + 4 * q + t;
+                const int j = c0 + 4 * q + t;
                 const float x = tanh_epi(v[4 * q + t] + b[j]);
                 hp[t] = tf32(x);
                 lp[t] = tf32(x - hp[t]);
             }
-            const uint32_t o = cm_off(row, 16 * c16 + 4 * q, H / 4);
+            const uint32_t o = cm_off(row, c0 + 4 * q, H / 4);
             *reinterpret_cast<float4*>(a_hi + o) = hi;
             *reinterpret_cast<float4*>(a_lo + o) = lo;
         }
@@ -768,12 +798,13 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     {
         float vp = 0.0f;
 #pragma unroll 1
-        for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
-            float v[16];
-            tmem_ld16(tacc + 16 * c16, v);
+        for (int cc = 0; cc < CPQ; ++cc) {
+            const int c0 = ch * CW + cc * CK;
+            float v[CK];
+            tmem_ld<CK>(tacc + c0, v);
 #pragma unroll
-            for (int t = 0; t < 16; ++t)
-                vp = fmaf(sp[S_CV + 16 * c16 + t], tanh_epi(v[t] + sp[S_B2C + 16 * c16 + t]), vp);
+            for (int t = 0; t < CK; ++t)
+                vp = fmaf(sp[S_CV + c0 + t], tanh_epi(v[t] + sp[S_B2C + c0 + t]), vp);
         }
         red[ch][row] = vp;
     }
@@ -781,8 +812,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();   // red complete; actor A_h complete
-    const float value = (NQ == 4 ? (red[0][row] + red[1][row]) + (red[NQ - 2][row] + red[NQ - 1][row])
-                                 : red[0][row] + red[1][row]) + sp[S_CVB];
+    const float value = sum_groups(red, row) + sp[S_CVB];
     // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
     // the mean head, over A_h once the actor's second layer has consumed it
     float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;
@@ -794,16 +824,17 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         mbar_wait(&bars[1], 0);   // A_h consumed: hrow may overwrite it
         tc_fence_after();
 #pragma unroll 1
-        for (int c16 = CPQ * ch; c16 < CPQ * ch + CPQ; ++c16) {
-            float v[16];
-            tmem_ld16(tacc + 16 * c16, v);
+        for (int cc = 0; cc < CPQ; ++cc) {
+            const int c0 = ch * CW + cc * CK;
+            float v[CK];
+            tmem_ld<CK>(tacc + c0, v);
 #pragma unroll
-            for (int t = 0; t < 16; t += 4)
-                *reinterpret_cast<float4*>(hrow + 16 * c16 + t) = make_float4(
-                    tanh_epi(v[t] + sp[S_B2A + 16 * c16 + t]),
-                    tanh_epi(v[t + 1] + sp[S_B2A + 16 * c16 + t + 1]),
-                    tanh_epi(v[t + 2] + sp[S_B2A + 16 * c16 + t + 2]),
-                    tanh_epi(v[t + 3] + sp[S_B2A + 16 * c16 + t + 3]));
+            for (int t = 0; t < CK; t += 4)
+                *reinterpret_cast<float4*>(hrow + c0 + t) = make_float4(
+                    tanh_epi(v[t] + sp[S_B2A + c0 + t]),
+                    tanh_epi(v[t + 1] + sp[S_B2A + c0 + t + 1]),
+                    tanh_epi(v[t + 2] + sp[S_B2A + c0 + t + 2]),
+                    tanh_epi(v[t + 3] + sp[S_B2A + c0 + t + 3]));
         }
     }
     tc_fence_before();
@@ -815,11 +846,11 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         if (active && ch == 0 && a.value_out) a.value_out[e] = value;
         return;
     }
-    // action dims: group ch takes Box-Muller pairs CPQ ch .. CPQ ch + CPQ - 1 (two dims each)
+    // action dims: group ch takes Box-Muller pairs PPQ ch .. PPQ ch + PPQ - 1 (two dims each)
     const uint64_t gid = a.env_offset + e;
     float logp = 0.0f;
 #pragma unroll 1
-    for (int p = CPQ * ch; p < CPQ * ch + CPQ; ++p) {
+    for (int p = PPQ * ch; p < PPQ * ch + PPQ; ++p) {
         if (2 * p >= A) break;
         float eps0 = 0.0f, eps1 = 0.0f;
         if (a.flags & 1) {   // Box-Muller on the counter-based stream
@@ -859,9 +890,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     red[ch][row] = logp;
     __syncthreads();
     if (active && ch == 0) {
-        if (a.logp_out)
-            a.logp_out[e] = NQ == 4 ? (red[0][row] + red[1][row]) + (red[NQ - 2][row] + red[NQ - 1][row])
-                                    : red[0][row] + red[1][row];
+        if (a.logp_out) a.logp_out[e] = sum_groups(red, row);
         if (a.value_out) a.value_out[e] = value;
     }
 }
