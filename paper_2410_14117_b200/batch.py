@@ -40,6 +40,7 @@ class B200EnvBatch:
     """M environments resident on one GPU, stepped by the fused sm_100a kernel."""
 
     backend = "b200"
+    _fast = None   # C fast path of step_ex (set with the pinned output pool)
 
     def __init__(self, config: dict | str, root_seed: int | None = None, threads: int = 0,
                  pinned: bool = True):
@@ -91,6 +92,17 @@ class B200EnvBatch:
     def step_ex(self, actions):
         """step() plus the termination reason per env (-1, 0 trunc, 1 div, 2 fail)."""
         self._require_open()
+        fast = self._fast
+        if fast is not None:
+            # C fast path (csrc/hostcall.c): float64 C-contiguous [M, A] actions straight
+            # into uuvsim_step_ex, outputs into a pooled block (anything else returns
+            # -100 and takes the general path below)
+            arrs, ptrs = self._free_block()
+            rc = fast(self._handle, actions, self.num_envs, self.action_dim, ptrs)
+            if rc == 0:
+                return arrs[0], arrs[1], arrs[2], arrs[3]
+            if rc != -100:
+                _core.check(self._lib, rc)
         act = np.ascontiguousarray(actions, dtype=np.float64)
         if act.shape != (self.num_envs, self.action_dim):
             raise ValueError(f"actions must have shape {(self.num_envs, self.action_dim)}, "
@@ -165,6 +177,7 @@ class B200EnvBatch:
         # step outputs: pool of pinned blocks [obs f64 | rew f64 | done u8 | reason i8]
         self._pool = []
         self._torch = torch
+        self._fast = _fast_step(self._lib)
 
     def _new_block(self):
         n, d = self.num_envs, self.obs_dim
@@ -387,6 +400,26 @@ def resolve_backend(backend: str | None = None) -> str:
         raise RuntimeError("this package is the B200 engine; the pure-Python backend lives in "
                            "the reference package (there is no CPU fallback here)")
     raise ValueError(f"unknown backend {choice!r}")
+
+
+_FAST = {}
+
+
+def _fast_step(lib):
+    """hostcall.step_ex bound to this library's uuvsim_step_ex, or None (module
+    not built, or a second library in the process: the ctypes path is used)."""
+    addr = ctypes.cast(lib.uuvsim_step_ex, ctypes.c_void_p).value
+    if addr not in _FAST:
+        fn = None
+        if not _FAST:   # the module holds one function pointer
+            try:
+                from . import _hostcall
+                _hostcall.bind(addr)
+                fn = _hostcall.step_ex
+            except ImportError:
+                fn = None
+        _FAST[addr] = fn
+    return _FAST[addr]
 
 
 def _pool_refs(entry):

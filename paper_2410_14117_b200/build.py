@@ -105,6 +105,8 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         for msg in ex.map(run, todo):
             if msg and verbose:
                 print(msg)
+    if out is None:
+        build_hostcall(force)
     objs = [str(o) for o, _, _ in jobs]
     if force or todo or _stale(lib, objs):
         cmd = [nvcc, "-shared", *ARCH, "-ccbin", cxx, "-o", str(lib), *objs,
@@ -113,6 +115,27 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     return lib
+
+
+def build_hostcall(force: bool = False) -> Path | None:
+    """CPython fast path of the host-ABI step (csrc/hostcall.c -> _hostcall<EXT>),
+    binding glue only; skipped (None) when the Python headers are absent."""
+    import sysconfig
+    inc = sysconfig.get_paths().get("include", "")
+    if not inc or not Path(inc, "Python.h").is_file():
+        return None
+    out = PKG / ("_hostcall" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+    src = CSRC / "hostcall.c"
+    if not force and not _stale(out, [src]):
+        return out
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        return None
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-Wall", "-I", inc, str(src), "-o", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"hostcall build failed:\n{r.stdout}\n{r.stderr}")
+    return out
 
 
 if __name__ == "__main__":
