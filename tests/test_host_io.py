@@ -158,3 +158,25 @@ def test_mapped_transport_with_misaligned_pinned_buffers():
         assert np.array_equal(done.astype(bool), dn)
     a.close()
     b.close()
+
+
+def test_fast_binding_equals_ctypes_path():
+    """B200EnvBatch.step through the CPython fast-call binding (csrc/hostcall.c)
+    and through ctypes (binding disabled) give bit-identical streams; inputs the
+    binding declines (float32, Fortran order, lists) take the general path."""
+    cfg = _cfg("lemniscate_dr", "auto")
+    a, b = uuv.B200EnvBatch(cfg, 5), uuv.B200EnvBatch(cfg, 5)
+    assert a._fast is not None, "hostcall extension not built"
+    b._fast = None
+    act = uuv.bench_actions(a)
+    variants = [act, act.astype(np.float32), np.asfortranarray(act), (0.5 * act).tolist()]
+    for k in range(24):
+        x = variants[k % len(variants)]
+        oa, ra, da, sa = a.step_ex(x)
+        ob, rb, db, sb = b.step_ex(x)
+        assert np.array_equal(oa, ob) and np.array_equal(ra, rb)
+        assert np.array_equal(da, db) and np.array_equal(sa, sb)
+    with pytest.raises(ValueError):
+        a.step(act[:10])
+    a.close()
+    b.close()
