@@ -127,6 +127,11 @@ int32_t uuvsim_dev_set_final_obs(uint64_t handle, void* buf, uint64_t len);
  * kernel-to-kernel launch gap.  Results are unchanged.  Host-ABI steps never
  * use it. */
 int32_t uuvsim_dev_set_pdl(uint64_t handle, int32_t on);
+/* register (buf != NULL) or clear (NULL) a caller-owned device buffer of
+ * num_envs floats: later device-face steps also write done as 0.0 / 1.0 into
+ * it (a rollout's done buffer, written by the step itself).  Not used by the
+ * host-buffer uuvsim_step. */
+int32_t uuvsim_dev_set_done_f32(uint64_t handle, float* buf, uint64_t len);
 /* PD baseline (reference baseline.py:38-75) over the engine's own state slab:
  * err_body = R^T (ref_xyz - p), err_ang = (ref_ang - ang + pi) mod 2 pi - pi,
  * wrench = kp * err - kd * nu, f = pinv(A) wrench, throttle = f / kmax (linear) or

@@ -59,6 +59,7 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
         "uuvsim_dev_states": (i32, [u64, vp, u64, u64]),
         "uuvsim_dev_set_final_obs": (i32, [u64, vp, u64]),
         "uuvsim_dev_set_pdl": (i32, [u64, i32]),
+        "uuvsim_dev_set_done_f32": (i32, [u64, vp, u64]),
         "uuvsim_dev_pd_actions": (i32, [u64, vp, vp, vp, u64, u64]),
         "uuvsim_snapshot_size": (i32, [u64, ctypes.POINTER(u64)]),
         "uuvsim_snapshot": (i32, [u64, vp, u64]),

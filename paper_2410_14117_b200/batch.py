@@ -291,19 +291,42 @@ class B200EnvBatch:
             self._stream(stream)))
         return t["obs"]
 
-    def step_tensors(self, actions, stream=None):
+    def step_tensors(self, actions, stream=None, rew_out=None):
         """One fused step on device tensors -> (obs, rew, done u8, reason i8) (reused).
 
-        Element dtype is ``self.dtype`` (float32 for the default fp32 engine)."""
+        Element dtype is ``self.dtype`` (float32 for the default fp32 engine).
+        ``rew_out``: a caller tensor of num_envs elements the reward goes to
+        instead (e.g. a rollout buffer row); it is returned as ``rew``."""
         self._require_open()
         self._check_actions(actions)
         t = self._tensors()
+        rew = t["rew"]
+        if rew_out is not None:
+            if (rew_out.dtype != rew.dtype or rew_out.numel() != rew.numel() or
+                    not rew_out.is_contiguous() or rew_out.device != rew.device):
+                raise ValueError(f"rew_out must be a contiguous {rew.dtype} tensor of "
+                                 f"{rew.numel()} elements on {rew.device}")
+            rew = rew_out
         _core.check(self._lib, self._lib.uuvsim_dev_step(
             self._handle, actions.data_ptr(), actions.numel(), t["obs"].data_ptr(),
-            t["obs"].numel(), t["rew"].data_ptr(), t["rew"].numel(), t["done"].data_ptr(),
+            t["obs"].numel(), rew.data_ptr(), rew.numel(), t["done"].data_ptr(),
             t["done"].numel(), t["reason"].data_ptr(), t["reason"].numel(),
             self._stream(stream)))
-        return t["obs"], t["rew"], t["done"], t["reason"]
+        return t["obs"], rew, t["done"], t["reason"]
+
+    def set_done_f32(self, buf) -> None:
+        """Register (tensor) or clear (None) a float32 [num_envs] device buffer
+        later device-face steps also write done into as 0.0 / 1.0
+        (uuvsim_dev_set_done_f32)."""
+        self._require_open()
+        if buf is None:
+            _core.check(self._lib, self._lib.uuvsim_dev_set_done_f32(self._handle, None, 0))
+            return
+        import torch
+        if buf.dtype != torch.float32 or not buf.is_cuda or not buf.is_contiguous():
+            raise ValueError("done buffer must be a contiguous float32 CUDA tensor")
+        _core.check(self._lib, self._lib.uuvsim_dev_set_done_f32(
+            self._handle, buf.data_ptr(), buf.numel()))
 
     def set_pdl(self, on: bool = True) -> None:
         """Launch later device-face steps as programmatic dependents of the previous

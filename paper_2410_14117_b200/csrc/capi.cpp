@@ -352,6 +352,18 @@ int32_t uuvsim_dev_set_final_obs(uint64_t h, void* buf, uint64_t len) {
     });
 }
 
+int32_t uuvsim_dev_set_done_f32(uint64_t h, float* buf, uint64_t len) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t want = (uint64_t)e.num_envs();
+        if (buf && len != want) return bad_size("done_f32", want, "f32");
+        if (buf) {
+            if (int32_t c = misaligned("done_f32", buf, 4)) return c;
+        }
+        e.dev_set_done_f32(buf);
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_dev_set_pdl(uint64_t h, int32_t on) {
     return with_engine(h, [&](uuv::Engine& e) {
         e.dev_set_pdl(on != 0);

@@ -474,6 +474,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.stats = stats_part_;
     p.vpack = d_vpack_;
     p.final_obs = nullptr;
+    p.done_f32 = nullptr;
     p.io_f64 = fp64_ ? 1 : 0;   // device face: engine precision; host ABI: set per launch
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are
     // already three 128-bit stores per env (measured)
@@ -747,15 +748,18 @@ void Engine::enqueue_step_host(const double* act, double* obs, double* rew, uint
                "step H2D");
     EngineP<T>& p = P<T>();
     p.io_f64 = 1;
-    void* const fo = p.final_obs;   // terminal obs and programmatic launch: device face only
+    void* const fo = p.final_obs;   // terminal obs, fp32 done, programmatic launch: device face only
+    float* const df = p.done_f32;
     const int32_t pdl = p.pdl;
     p.final_obs = nullptr;
+    p.done_f32 = nullptr;
     p.pdl = 0;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           d_act64_, d_obs64_, d_rew64_, d_done_, d_reason_,
                                           stream_);
     p.io_f64 = fp64_ ? 1 : 0;
     p.final_obs = fo;
+    p.done_f32 = df;
     p.pdl = pdl;
     cuda_check(e, "step");
     cuda_check(cudaMemcpyAsync(obs, d_obs64_, n_obs * 8, cudaMemcpyDeviceToHost, stream_), "obs D2H");
@@ -824,8 +828,10 @@ void Engine::enqueue_step_mapped() {
     EngineP<T>& p = P<T>();
     const int32_t io = p.io_f64, stage = p.stage_obs, pdl = p.pdl;
     void* const fo = p.final_obs;
+    float* const df = p.done_f32;
     p.io_f64 = 1;
     p.final_obs = nullptr;
+    p.done_f32 = nullptr;
     p.pdl = 0;
     p.stage_obs = obs_dim_ <= MAX_STAGE_DIM ? 1 : 0;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
@@ -835,6 +841,7 @@ void Engine::enqueue_step_mapped() {
     p.io_f64 = io;
     p.stage_obs = stage;
     p.final_obs = fo;
+    p.done_f32 = df;
     p.pdl = pdl;
     cuda_check(e, "step (mapped)");
 }
@@ -1097,6 +1104,11 @@ void Engine::dev_observe(void* obs, cudaStream_t st) {
     check_device();
     if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
+}
+
+void Engine::dev_set_done_f32(float* buf) {
+    if (fp64_) pd_->done_f32 = buf;
+    else pf_->done_f32 = buf;
 }
 
 void Engine::dev_set_pdl(bool on) {

@@ -101,6 +101,7 @@ public:
     void dev_pd_actions(const UuvPdGains& g, const void* ref6, void* act, cudaStream_t st);
     void dev_set_final_obs(void* buf);
     void dev_set_pdl(bool on);
+    void dev_set_done_f32(float* buf);
     void dev_stats(double* out, bool clear, cudaStream_t st);
     void graph_capture(const void* act, void* obs, void* rew, uint8_t* done, int8_t* reason,
                        int n_steps);

@@ -981,7 +981,9 @@ int32_t uuvsim_rl_post(const UuvRlPostArgs* a, uint64_t stream) {
     if (!a || a->num_envs == 0 || a->obs_dim > 36 || (a->n_part && (!a->stats_part ||
         !a->norm_mean || !a->norm_var || !a->norm_count)))
         return 3;
-    const unsigned grid = (unsigned)(1 + (a->num_envs + 1023) / 1024);   // + statistics block
+    const bool copy = (a->rew_in && a->rew_out) || (a->done_in && a->done_out);
+    const unsigned grid = copy ? (unsigned)(1 + (a->num_envs + 1023) / 1024)   // + statistics block
+                               : 1u;
     const cudaError_t e = uuvrl::launch_k(uuvrl::k_rl_post, grid, 1024, 0,
                                           reinterpret_cast<cudaStream_t>(stream),
                                           (a->flags & 1) != 0, *a);

@@ -198,6 +198,9 @@ template <class T> struct EngineP {
     // optional [n_env][obs_dim] T buffer (device face): finished envs write their
     // TERMINAL observation (pre-reset state at the terminating step) here
     void* final_obs;
+    // optional [n_env] fp32 buffer (device face): done as 0 / 1 floats, e.g. a
+    // rollout's done buffer written by the step itself
+    float* done_f32;
 };
 
 constexpr int PACK_F4 = 10;   // 40 floats: Fossen pattern + restoring + trig constants

@@ -275,6 +275,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
         ((T*)rew)[e] = reward;
     }
     done[e] = rc >= 0 ? 1 : 0;
+    if (p.done_f32) p.done_f32[e] = rc >= 0 ? 1.0f : 0.0f;
     if (reason) reason[e] = (int8_t)rc;
     st.rew += (float)reward;
     st.n_act += 1;

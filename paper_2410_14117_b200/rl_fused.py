@@ -110,9 +110,12 @@ class FusedActorCritic:
 
     def post(self, rew=None, done=None, rew_out=None, done_out=None, update_norm: bool = True):
         nm = self.norm
+        # programmatic launch only behind the env step on the same stream (a bare
+        # statistics merge runs on a side stream of the collection graph)
+        pdl = self.pdl and rew is not None
         a = PostArgs(self.M, self.D, self.n_part if update_norm else 0, _p(self.stats_part),
                      _p(nm.mean), _p(nm.var), _p(nm.count), _p(rew), _p(done), _p(rew_out),
-                     _p(done_out), _p(self.noise_ctr), 1 if self.pdl else 0, 0)
+                     _p(done_out), _p(self.noise_ctr), 1 if pdl else 0, 0)
         _core.check(self.lib, self.lib.uuvsim_rl_post(
             ctypes.byref(a), torch.cuda.current_stream().cuda_stream))
 

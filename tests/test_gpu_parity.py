@@ -310,6 +310,32 @@ def test_programmatic_launch_step_is_bit_identical(n, pair):
     b.close()
 
 
+def test_reward_into_caller_buffer_and_fp32_done():
+    """step_tensors(rew_out=...) + set_done_f32: the reward lands in the caller's
+    row, done is also written as 0/1 floats; everything else unchanged."""
+    cfg = _cfg(kind="circle", n=5000, episode_len=9)
+    a, b = uuv.B200EnvBatch(cfg), uuv.B200EnvBatch(cfg)
+    act = a.bench_actions_tensor()
+    rows = torch.zeros((12, 5000), device="cuda")
+    dones = torch.full((12, 5000), 7.0, device="cuda")
+    for k in range(12):
+        a.set_done_f32(dones[k])
+        oa, ra, da, sa = a.step_tensors(act, rew_out=rows[k])
+        ob, rb, db, sb = b.step_tensors(act)
+        assert ra.data_ptr() == rows[k].data_ptr()
+        assert torch.equal(oa, ob) and torch.equal(ra, rb) and torch.equal(da, db)
+        assert torch.equal(dones[k], db.float())
+    a.set_done_f32(None)
+    a.step_tensors(act)
+    torch.cuda.synchronize()
+    assert torch.equal(dones[-1], db.float())            # cleared: no further writes
+    assert int(dones.sum().item()) > 0                   # episode_len 9: truncations seen
+    with pytest.raises(ValueError):
+        a.step_tensors(act, rew_out=torch.zeros(10, device="cuda"))
+    a.close()
+    b.close()
+
+
 def test_sharding_invariance_on_device():
     whole_cfg = _cfg(kind="helix", dr="episode", episode_len=50, n=6000, seed=4)
     halves = [_cfg(kind="helix", dr="episode", episode_len=50, n=3000, seed=4, env_offset=o)
