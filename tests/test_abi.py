@@ -70,6 +70,11 @@ def test_invalid_handle_paths(lib):
     assert lib.uuvsim_states(987654321, buf, 4) == 2
     assert lib.uuvsim_set_threads(987654321, 0) == 2
     assert lib.uuvsim_step(987654321, None, 0, None, 0, None, 0, None, 0) == 2
+    # B200 device-face extensions reject a stale handle the same way (no device work)
+    assert lib.uuvsim_dev_set_pdl(987654321, 1) == 2
+    assert lib.uuvsim_dev_set_done_f32(987654321, None, 0) == 2
+    assert lib.uuvsim_dev_set_final_obs(987654321, None, 0) == 2
+    assert "not valid" in _err(lib)
 
 
 def test_last_error_contract(lib):
