@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "uuv_common.cuh"
+#include "launch_kernel.cuh"
 #include "../../include/uuvsim_rl.h"
 
 #ifndef UUV_PDL_TRIGGER
@@ -330,27 +331,6 @@ __global__ void k_rl_post(const UuvRlPostArgs a) {
         if (threadIdx.x == 0) *a.norm_count = tot_sh;
     }
     if (threadIdx.x == 0 && a.noise_ctr) *a.noise_ctr += 1;
-}
-
-// <<<>>> launch, or cudaLaunchKernelEx with programmatic stream serialisation
-template <class... KArgs, class... Args>
-static cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
-                            cudaStream_t st, bool pdl, Args... args) {
-    if (!pdl) {
-        k<<<grid, block, smem, st>>>(args...);
-        return cudaSuccess;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 // dynamic shared memory opt-in, once per kernel and device (attributes are per
@@ -968,7 +948,7 @@ int32_t uuvsim_rl_policy_act(const UuvRlPolicyArgs* a, uint64_t stream) {
         const size_t smem = uuvtc::smem_bytes((int)a->obs_dim);
         uuvrl::smem_optin<uuvtc::k_policy_tc>((int)uuvtc::smem_bytes(36));
         const unsigned grid = (unsigned)((a->num_envs + uuvtc::M - 1) / uuvtc::M);
-        const cudaError_t e = uuvrl::launch_k(uuvtc::k_policy_tc, grid, uuvtc::NT, smem, st,
+        const cudaError_t e = uuv::launch_k(uuvtc::k_policy_tc, dim3(grid), dim3(uuvtc::NT), smem, st,
                                               (a->flags & 8) != 0, *a);
         return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 4;
     }
@@ -984,7 +964,7 @@ int32_t uuvsim_rl_post(const UuvRlPostArgs* a, uint64_t stream) {
     const bool copy = (a->rew_in && a->rew_out) || (a->done_in && a->done_out);
     const unsigned grid = copy ? (unsigned)(1 + (a->num_envs + 1023) / 1024)   // + statistics block
                                : 1u;
-    const cudaError_t e = uuvrl::launch_k(uuvrl::k_rl_post, grid, 1024, 0,
+    const cudaError_t e = uuv::launch_k(uuvrl::k_rl_post, dim3(grid), dim3(1024), 0,
                                           reinterpret_cast<cudaStream_t>(stream),
                                           (a->flags & 1) != 0, *a);
     return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : 4;

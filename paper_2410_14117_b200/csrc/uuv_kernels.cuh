@@ -21,6 +21,7 @@
 
 #include "uuv_model.cuh"
 #include "launch.h"
+#include "launch_kernel.cuh"
 
 namespace uuv {
 
@@ -844,27 +845,6 @@ static void allow_smem() {
     if (done.load(std::memory_order_acquire) & bit) return;
     cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_STAGE_BYTES);
     done.fetch_or(bit, std::memory_order_release);
-}
-
-// <<<>>> launch, or cudaLaunchKernelEx with programmatic stream serialisation
-template <class... KArgs, class... Args>
-static cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                            cudaStream_t st, bool pdl, Args... args) {
-    if (!pdl) {
-        k<<<grid, block, smem, st>>>(args...);
-        return cudaSuccess;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
 template <class T>
