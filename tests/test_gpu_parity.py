@@ -58,6 +58,11 @@ CONFIGS = {
     "mixed_circle_pair": dict(kind="circle", mixed=True, episode_len=33, pair="on", n=4000),
     "station_heavy_dense": dict(pattern="dense", episode_len=29),
     "circle_dense_drep": dict(kind="circle", pattern="dense", dr="episode", episode_len=23),
+    # lookahead outside the prefetched / staged range: 1 row (obs_dim 12) and 8 rows
+    # (obs_dim 54 > the 36-float staging limit: direct stores, table loop)
+    "circle_lookahead1": dict(kind="circle", vehicle="bluerov2", lookahead=1, episode_len=31),
+    "lemniscate_lookahead8_drep": dict(kind="lemniscate", lookahead=8, dr="episode",
+                                       episode_len=27),
 }
 
 
