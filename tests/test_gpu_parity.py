@@ -173,7 +173,8 @@ def test_single_step_teacher_forced(name):
     assert n_checked > 0.95 * n_steps * gpu.num_envs - n_band
 
 
-@pytest.mark.parametrize("name", ["station_heavy", "lemniscate_heavy_drep", "mixed_station_dr"])
+@pytest.mark.parametrize("name", ["station_heavy", "lemniscate_heavy_drep", "mixed_station_dr",
+                                  "circle_3sub_fast", "lemniscate_lookahead8_drep"])
 def test_rollout_drift_and_exact_terminations(name):
     """100 free-running steps: terminations / counters bit-exact, state drift bounded."""
     cfg = _cfg(**CONFIGS[name])
