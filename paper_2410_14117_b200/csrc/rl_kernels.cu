@@ -407,6 +407,18 @@ __host__ __device__ inline uint32_t cm_off(int row, int k, int KC) {
     return (uint32_t)((((row >> 3) * KC + (k >> 2)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
 }
 
+#ifndef UUV_TC_STOP
+#define UUV_TC_STOP 0   // phase probe (tools/c4_loop_probe.py): 1-4 return after that phase
+#endif
+#define UUV_TC_EXIT_AFTER(n)                                                                    \
+    if (UUV_TC_STOP == (n)) {                                                                 \
+        tc_fence_before();                                                                    \
+        __syncthreads();                                                                      \
+        if (warp == 0)                                                                        \
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem)); \
+        return;                                                                               \
+    }
+
 #ifndef UUV_TC_FAST_TANH
 #define UUV_TC_FAST_TANH 1
 #endif
@@ -608,6 +620,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     __shared__ uint32_t tmem_base_sh;
     __shared__ double nsc[2 * 36];              // normaliser mean, 1 / sqrt(var + 1e-8)
     __shared__ float red[NQ][M];                // cross-group partials
+    __shared__ double gstat[NT];                // normaliser sums per (row group, column)
     const int D = (int)a.obs_dim, A = (int)a.act_dim;
     const bool value_only = (a.flags & 4) != 0;
     const Img g = img_layout(D);
@@ -638,6 +651,27 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     // (observations, normaliser statistics, noise counter, weight image) is read
     // before this point
     if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    // ---- observations: issued first (one memory round trip for the rows, the
+    // running statistics and the noise counter together), stored to shared memory
+    // after the barrier that publishes the TMEM base
+    const uint64_t e = (uint64_t)blockIdx.x * M + row;
+    const bool active = e < a.num_envs;
+    float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][D] (A_h unused yet)
+    const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
+    const int nvalid = left < (uint64_t)M ? (int)left : M;
+    const float* src = a.obs + (uint64_t)blockIdx.x * M * D;
+    const int nf = nvalid * D;
+    constexpr int PER = (M * 36 / 4 + NT - 1) / NT;   // float4 per thread at D = 36
+    const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const int n4 = vec ? nf >> 2 : 0;
+    float4 buf[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int i = tid + j * NT;
+        buf[j] = i < n4 ? __ldg(reinterpret_cast<const float4*>(src) + i) : float4{};
+    }
+    const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;
     if (tid < D) {
         nsc[tid] = a.norm_mean[tid];
         nsc[36 + tid] = 1.0 / sqrt(a.norm_var[tid] + 1e-8);
@@ -646,65 +680,46 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
-    if (tid == 0) {   // the whole weight image in one bulk copy
+    if (UUV_TC_STOP == 8) {   // probe: launch + TMEM alloc only
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+        return;
+    }
+    if (tid == 0 && UUV_TC_STOP != 7) {   // the whole weight image in one bulk copy
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                      ::"r"(s_u32(&bars[0])), "r"(g.total) : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
             ::"r"(s_u32(wimg)), "l"(a.wimage), "r"(g.total), "r"(s_u32(&bars[0])) : "memory");
     }
-
-    // ---- observations: normaliser sums, normalise + clip, A_z, nobs_out
-    const uint64_t e = (uint64_t)blockIdx.x * M + row;
-    const bool active = e < a.num_envs;
-    const uint64_t ctr = a.noise_ctr ? *a.noise_ctr : 0;   // issued early: one round trip
-    float* raw = reinterpret_cast<float*>(ah_hi);        // scratch [128][D] (A_h unused yet)
-    const uint64_t left = a.num_envs - (uint64_t)blockIdx.x * M;
-    const int nvalid = left < (uint64_t)M ? (int)left : M;
-    {   // the CTA's rows are one contiguous span in global AND shared memory: a
-        // straight coalesced copy, every 16-byte load issued before any store
-        const float* src = a.obs + (uint64_t)blockIdx.x * M * D;
-        const int nf = nvalid * D;
-        constexpr int PER = (M * 36 / 4 + NT - 1) / NT;   // float4 per thread at D = 36
-        int done_f = 0;
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            const int n4 = nf >> 2;
-            float4 buf[PER];
+    {   // the CTA's rows are one contiguous span in global AND shared memory
 #pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const int i = tid + j * NT;
-                buf[j] = i < n4 ? __ldg(reinterpret_cast<const float4*>(src) + i) : float4{};
-            }
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const int i = tid + j * NT;
-                if (i < n4) reinterpret_cast<float4*>(raw)[i] = buf[j];
-            }
-            done_f = n4 << 2;
+        for (int j = 0; j < PER; ++j) {
+            const int i = tid + j * NT;
+            if (i < n4) reinterpret_cast<float4*>(raw)[i] = buf[j];
         }
-        for (int f = done_f + tid; f < nf; f += NT) raw[f] = __ldg(src + f);
+        for (int f = (n4 << 2) + tid; f < nf; f += NT) raw[f] = __ldg(src + f);
         for (int f = nf + tid; f < M * D; f += NT) raw[f] = 0.0f;   // rows past the last env
     }
     __syncthreads();
-    if ((a.flags & 2) && tid < 2 * D) {
-        const int d = tid < D ? tid : tid - D;
-        // four interleaved partial sums (fixed order: deterministic) shorten the
-        // fp64 dependency chain 4x
-        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-        int r = 0;
-        for (; r + 4 <= nvalid; r += 4) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const double v = raw[(r + q) * D + d];
-                acc4[q] += tid < D ? v : v * v;
+    // normaliser sums: thread (g, c) adds column c (sum x | sum x^2) over rows g,
+    // g + G, ... (G = NT / 2 D groups); the group partials are added in group order
+    // after the next barrier (fixed order: deterministic)
+    const int ncol = 2 * D, ngrp = NT / ncol;
+    const bool stats = (a.flags & 2) != 0;
+    if (stats) {
+        const int sg = tid / ncol, sc = tid - sg * ncol;
+        if (sg < ngrp) {
+            const int d = sc < D ? sc : sc - D;
+            double acc = 0.0;
+            for (int r = sg; r < nvalid; r += ngrp) {
+                const double v = raw[r * D + d];
+                acc += sc < D ? v : v * v;
             }
+            gstat[tid] = acc;
         }
-        for (; r < nvalid; ++r) {
-            const double v = raw[r * D + d];
-            acc4[0] += tid < D ? v : v * v;
-        }
-        const double acc = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-        a.stats_part[(size_t)blockIdx.x * 2 * D + tid] = acc;   // one row per CTA
     }
     // normalise: the two column halves split the K chunks; the fp32 rows are staged
     // in A_h's lo half (unused yet) and stored to nobs_out coalesced afterwards
@@ -733,10 +748,17 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // A_z -> tensor-core proxy
     __syncthreads();
+    UUV_TC_EXIT_AFTER(7)   // probe: load + normalise, no weight image
     mbar_wait(&bars[0], 0);                                        // weights landed
+    UUV_TC_EXIT_AFTER(1)   // probe: load + normalise + weight image
     if (tid == 0) {   // round 1: critic layer 1 (runs while the normalised rows go out)
         tc_fence_after();
         issue_layer(tmem, az_hi, az_lo, wimg + g.w1c_hi, wimg + g.w1c_lo, K1, &bars[1]);
+    }
+    if (stats && tid < ncol) {   // this CTA's partial row of the normaliser sums
+        double acc = 0.0;
+        for (int q = 0; q < ngrp; ++q) acc += gstat[q * ncol + tid];
+        a.stats_part[(size_t)blockIdx.x * 2 * D + tid] = acc;
     }
     if (a.nobs_out) {   // the CTA's normalised rows: one contiguous span
         float* dst = a.nobs_out + (uint64_t)blockIdx.x * M * D;
@@ -766,6 +788,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
+    UUV_TC_EXIT_AFTER(2)   // probe: + round 1 and its epilogue
     if (tid == 0) {   // round 2: critic layer 2 (acc0) + actor layer 1 (acc1), one commit
         tc_fence_after();
         if (!value_only)
@@ -793,6 +816,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     tc_fence_before();
     __syncthreads();   // red complete; actor A_h complete
     const float value = sum_groups(red, row) + sp[S_CVB];
+    UUV_TC_EXIT_AFTER(3)   // probe: + round 2 and its epilogues
     // actor trunk output parked in fp32 rows (stride 68: conflict-free float4 reads) for
     // the mean head, over A_h once the actor's second layer has consumed it
     float* hrow = reinterpret_cast<float*>(ah_hi) + row * 68;
@@ -822,6 +846,7 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     if (UUV_PDL_TRIGGER == 2 && pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+    if (UUV_TC_STOP == 4) return;   // probe: + round 3 and its epilogue
     if (value_only) {
         if (active && ch == 0 && a.value_out) a.value_out[e] = value;
         return;
