@@ -704,6 +704,8 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
         for (int f = nf + tid; f < M * D; f += NT) raw[f] = 0.0f;   // rows past the last env
     }
     __syncthreads();
+    if (UUV_TC_STOP == 9) mbar_wait(&bars[0], 0);
+    UUV_TC_EXIT_AFTER(9)   // probe: + observation rows in shared memory
     // normaliser sums: thread (g, c) adds column c (sum x | sum x^2) over rows g,
     // g + G, ... (G = NT / 2 D groups); the group partials are added in group order
     // after the next barrier (fixed order: deterministic)
@@ -748,6 +750,8 @@ __global__ void __launch_bounds__(NT, 1) k_policy_tc(const UuvRlPolicyArgs a) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // A_z -> tensor-core proxy
     __syncthreads();
+    if (UUV_TC_STOP == 10) mbar_wait(&bars[0], 0);
+    UUV_TC_EXIT_AFTER(10)   // probe: + normaliser sums and normalisation
     UUV_TC_EXIT_AFTER(7)   // probe: load + normalise, no weight image
     mbar_wait(&bars[0], 0);                                        // weights landed
     UUV_TC_EXIT_AFTER(1)   // probe: load + normalise + weight image
