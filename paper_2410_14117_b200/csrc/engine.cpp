@@ -2,6 +2,7 @@
 // launches).  See engine.h for the reference mapping.
 #include "engine.h"
 
+#include <algorithm>
 #include <array>
 #include <climits>
 #include <cmath>
@@ -834,6 +835,10 @@ void Engine::enqueue_step_mapped() {
     p.done_f32 = nullptr;
     p.pdl = 0;
     p.stage_obs = obs_dim_ <= MAX_STAGE_DIM ? 1 : 0;
+    // stagger block starts over ~half the action read time on the host link (bytes/100
+    // ~ ns at ~50 GB/s, capped at 2 us): early blocks' observation writes overlap the
+    // later blocks' action reads (link is full duplex).  Measured, DESIGN.md §5
+    p.stagger_ns = (int32_t)std::min<size_t>(2000, (size_t)m_ * n_act_ * 8 / 100);
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           dev_io_[0], dev_io_[1], dev_io_[2],
                                           (uint8_t*)dev_io_[3], (int8_t*)dev_io_[4],
@@ -843,6 +848,7 @@ void Engine::enqueue_step_mapped() {
     p.final_obs = fo;
     p.done_f32 = df;
     p.pdl = pdl;
+    p.stagger_ns = 0;
     cuda_check(e, "step (mapped)");
 }
 

@@ -497,6 +497,7 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
     pdl_enter(p.pdl != 0);
+    if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     StatAcc st;
     if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
@@ -517,6 +518,7 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
             void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
             int8_t* __restrict__ reason) {
     pdl_enter(p.pdl != 0);
+    if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
     StatAcc st;
     const bool a0 = e0 < p.n_env, a1 = e1 < p.n_env;
