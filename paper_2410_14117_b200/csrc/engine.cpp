@@ -839,6 +839,10 @@ void Engine::enqueue_step_mapped() {
     // ~ ns at ~50 GB/s, capped at 2 us): early blocks' observation writes overlap the
     // later blocks' action reads (link is full duplex).  Measured, DESIGN.md §5
     p.stagger_ns = (int32_t)std::min<size_t>(2000, (size_t)m_ * n_act_ * 8 / 100);
+    // action rows through shared memory once the read is bandwidth-bound on the link
+    // (measured: 16,384 envs 61.6 -> 57.6 us; 512 / 4,096 envs +1 us, latency-bound:
+    // threads that start on their own row overlap the stragglers' loads)
+    p.stage_act = (size_t)m_ * n_act_ * 8 >= (size_t(512) << 10) ? 1 : 0;
     const cudaError_t e = Launch<T>::step(p, task_.kind != 0, ranges_.enabled, fossen_, pair_,
                                           dev_io_[0], dev_io_[1], dev_io_[2],
                                           (uint8_t*)dev_io_[3], (int8_t*)dev_io_[4],
@@ -849,6 +853,7 @@ void Engine::enqueue_step_mapped() {
     p.done_f32 = df;
     p.pdl = pdl;
     p.stagger_ns = 0;
+    p.stage_act = 0;
     cuda_check(e, "step (mapped)");
 }
 

@@ -64,7 +64,8 @@ constexpr int TMA_MIN_BLOCKS = UUV_TMA_MIN_BLOCKS;
 
 // observation staging in shared memory: obs_dim <= MAX_STAGE_DIM (lookahead <= 5)
 constexpr int MAX_STAGE_DIM = 36;
-constexpr int MAX_STAGE_BYTES = 2 * BLOCK * MAX_STAGE_DIM * 8;   // paired block, f64 rows
+constexpr int MAX_STAGE_BYTES = 2 * BLOCK * MAX_STAGE_DIM * 8    // paired block, f64 rows
+                                + 2 * BLOCK * 8 * 8;              // + staged f64 action rows
 
 template <class T> struct Launch {
     // one fused step; fossen selects the structure-specialised variant, pair the

@@ -201,6 +201,7 @@ template <class T> struct EngineP {
     // optional [n_env] fp32 buffer (device face): done as 0 / 1 floats, e.g. a
     // rollout's done buffer written by the step itself
     float* done_f32;
+    int32_t stage_act;     // host-ABI zero-copy step: f64 action rows staged in shared memory
     int32_t stagger_ns;    // host-ABI zero-copy step: block b starts b*stagger_ns/gridDim ns late
 };
 

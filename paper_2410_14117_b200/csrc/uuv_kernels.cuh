@@ -489,6 +489,36 @@ __device__ __forceinline__ void flush_obs(const EngineP<T>& p, void* __restrict_
     }
 }
 
+// Host-ABI zero-copy step (EngineP::stage_act): the block's f64 action rows are
+// read from the mapped page-locked buffer with consecutive 8-byte loads (each warp
+// instruction covers 256 contiguous bytes, whole lines on the host link, instead of
+// six 48-byte-strided loads per env) into shared memory behind the staged
+// observation rows.  Returns the base act_row() offsets by the block's env index.
+template <class T>
+__device__ __forceinline__ const void* stage_actions(const EngineP<T>& p, const void* act,
+                                                     int first, int n, int rows) {
+    const size_t obs_bytes = p.stage_obs ? (size_t)rows * p.task.obs_dim * 8 : 0;
+    double* sa = reinterpret_cast<double*>(uuv_smem + obs_bytes);
+    const double* src = static_cast<const double*>(act) + (size_t)first * p.act_dim;
+    const int cnt = n * p.act_dim;
+    // all loads in flight before the first store: a load -> store loop would pay
+    // one host-link round trip per iteration
+    double v[2 * MAX_THR];
+#pragma unroll
+    for (int k = 0; k < 2 * MAX_THR; ++k) {
+        const int i = threadIdx.x + k * BLOCK;
+        if (i < cnt) v[k] = src[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * MAX_THR; ++k) {
+        const int i = threadIdx.x + k * BLOCK;
+        if (i < cnt) sa[i] = v[k];
+    }
+    __syncthreads();
+    return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(sa) -
+                                         (uintptr_t)first * p.act_dim * sizeof(double));
+}
+
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BLOCK, is_f64<T>() ? STEP_MIN_BLOCKS_F64
                                       : (DR ? (Pat::fossen ? STEP_MIN_BLOCKS_DR : STEP_MIN_BLOCKS_F64)
@@ -499,6 +529,10 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
     pdl_enter(p.pdl != 0);
     if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e = blockIdx.x * BLOCK + threadIdx.x;
+    if (p.stage_act) {
+        const int first = blockIdx.x * BLOCK;
+        act = stage_actions(p, act, first, min(BLOCK, p.n_env - first), BLOCK);
+    }
     StatAcc st;
     if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
                                                      reason, st);
@@ -520,6 +554,10 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     pdl_enter(p.pdl != 0);
     if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
+    if (p.stage_act) {
+        const int first = blockIdx.x * (2 * BLOCK);
+        act = stage_actions(p, act, first, min(2 * BLOCK, p.n_env - first), 2 * BLOCK);
+    }
     StatAcc st;
     const bool a0 = e0 < p.n_env, a1 = e1 < p.n_env;
     const int sl0 = MIX && (int64_t)(p.env_offset + (uint64_t)e0) >= p.mix_bound0;
@@ -871,7 +909,8 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
         }
         if (pair && fossen && !dr) {
             const dim3 grid((p.n_env + 2 * BLOCK - 1) / (2 * BLOCK));
-            const size_t smem = p.stage_obs ? (size_t)2 * BLOCK * p.task.obs_dim * esz : 0;
+            const size_t smem = (p.stage_obs ? (size_t)2 * BLOCK * p.task.obs_dim * esz : 0) +
+                                (p.stage_act ? (size_t)2 * BLOCK * p.act_dim * 8 : 0);
 #define UUV_P(TR, M)                                                                   \
     do {                                                                               \
         allow_smem<k_step_pair<TR, M>>();                                              \
@@ -886,7 +925,8 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
         }
     }
     const dim3 grid((p.n_env + BLOCK - 1) / BLOCK);
-    const size_t smem = p.stage_obs ? (size_t)BLOCK * p.task.obs_dim * esz : 0;
+    const size_t smem = (p.stage_obs ? (size_t)BLOCK * p.task.obs_dim * esz : 0) +
+                        (p.stage_act ? (size_t)BLOCK * p.act_dim * 8 : 0);
 #define UUV_L(TR, D, M, PAT)                                                                 \
     do {                                                                                     \
         allow_smem<k_step<T, TR, D, M, PAT>>();                                              \

@@ -20,6 +20,11 @@ CASES = {
     "station_heavy": dict(kind="station_keeping", dr=False, n=4096, L=37),
     "lemniscate_dr": dict(kind="lemniscate", dr=True, n=3000, L=29),
     "circle_big": dict(kind="circle", dr=False, n=140000, L=23),   # pair kernel, staged rows
+    # zero-copy with the action rows staged through shared memory (>= 512 KiB of
+    # actions): paired station kernel, and the DR tracking kernel with a ragged
+    # last block and staged observation rows in front of the action rows
+    "station_16k": dict(kind="station_keeping", dr=False, n=16384, L=31),
+    "lemniscate_dr_10k": dict(kind="lemniscate", dr=True, n=10000, L=27),
 }
 
 
