@@ -77,7 +77,7 @@ def bytes_per_env_step(kind: str, n_act: int, obs_dim: int, dr: bool) -> int:
 
 
 def build_config(name: str, rank: int, precision: str, pair: str = "auto",
-                 stage_obs: str = "auto"):
+                 stage_obs: str = "auto", band64: bool = True):
     import paper_2410_14117_b200 as uuv
     c = CONFIGS[name]
     n = c["num_envs"]
@@ -96,6 +96,7 @@ def build_config(name: str, rank: int, precision: str, pair: str = "auto",
                                      device=rank_device(), env_offset=rank * n)
     cfg["device"]["pair"] = pair
     cfg["device"]["stage_obs"] = stage_obs
+    cfg["device"]["band64"] = band64
     return cfg, [v.n_thrusters() for v in vdocs]
 
 
@@ -289,6 +290,8 @@ def main():
                     help="two envs per thread (default: auto by env count)")
     ap.add_argument("--stage-obs", default="auto", choices=["auto", "on", "off"],
                     help="observation rows through shared memory (default: tracking only)")
+    ap.add_argument("--band64", default="on", choices=["on", "off"],
+                    help="fp64 recompute of steps whose pitch leaves |theta| <= 1.4 (default on)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the secondary config sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
@@ -319,7 +322,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    cfg, n_thr = build_config(args.config, rank, args.precision, args.pair, args.stage_obs)
+    cfg, n_thr = build_config(args.config, rank, args.precision, args.pair, args.stage_obs,
+                             args.band64 == "on")
     c = CONFIGS[args.config]
     env = uuv.B200EnvBatch(cfg)
     n = env.num_envs
@@ -448,7 +452,8 @@ def main():
         for name in ("c4", "c3", "c3_circle", "c3_helix", "c5"):
             if name == args.config:
                 continue
-            cfg2, nt2 = build_config(name, rank, args.precision, args.pair, args.stage_obs)
+            cfg2, nt2 = build_config(name, rank, args.precision, args.pair, args.stage_obs,
+                                    args.band64 == "on")
             e2 = uuv.B200EnvBatch(cfg2)
             a2 = e2.bench_actions_tensor()
             e2.capture_graph(a2, n_steps=1)

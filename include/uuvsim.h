@@ -89,9 +89,11 @@ int32_t uuvsim_counters(uint64_t handle, uint64_t* reset_ctr, uint64_t* param_ct
 /* per-env randomised parameter record [M][10]:
  * f_mass f_added f_dlin f_dquad f_thrust rb_x rb_y rb_z weight buoyancy */
 int32_t uuvsim_dr_factors(uint64_t handle, double* out, uint64_t len);
-/* episode statistics [8]: sum reward, dones by reason (trunc, div, fail),
+/* episode statistics [9]: sum reward, dones by reason (trunc, div, fail),
  * sum of completed-episode returns, sum of their lengths, env-steps,
- * rejected per-episode resamples.  clear != 0 zeroes the accumulators. */
+ * rejected per-episode resamples, fp32 env-steps recomputed in fp64 because
+ * their pitch left |theta| <= 1.4 (Euler band).  clear != 0 zeroes the
+ * accumulators. */
 int32_t uuvsim_stats(uint64_t handle, double* out, uint64_t len, int32_t clear);
 /* JSON description of the engine (precision, grid, registers, device) */
 int64_t uuvsim_info(uint64_t handle, char* buf, uint64_t cap);

@@ -29,7 +29,8 @@ from .config import (ConfigError, RandomizationRanges, TaskSpec, VehicleParams,
                      engine_config_dict)
 
 STAT_NAMES = ("sum_reward", "done_truncation", "done_divergence", "done_failure",
-              "sum_episode_return", "sum_episode_length", "env_steps", "resample_rejected")
+              "sum_episode_return", "sum_episode_length", "env_steps", "resample_rejected",
+              "band64_steps")
 
 
 def _ptr(a: np.ndarray):
@@ -229,8 +230,8 @@ class B200EnvBatch:
         return out
 
     def stats(self, clear: bool = False) -> dict:
-        out = np.zeros(8)
-        _core.check(self._lib, self._lib.uuvsim_stats(self._handle, _ptr(out), 8, int(clear)))
+        out = np.zeros(len(STAT_NAMES))
+        _core.check(self._lib, self._lib.uuvsim_stats(self._handle, _ptr(out), len(STAT_NAMES), int(clear)))
         return dict(zip(STAT_NAMES, out.tolist()))
 
     def _info(self) -> str:
@@ -255,7 +256,7 @@ class B200EnvBatch:
                 "rew": torch.zeros(n, dtype=dt, device=dev),
                 "done": torch.zeros(n, dtype=torch.uint8, device=dev),
                 "reason": torch.zeros(n, dtype=torch.int8, device=dev),
-                "stats": torch.zeros(8, dtype=torch.float64, device=dev),
+                "stats": torch.zeros(len(STAT_NAMES), dtype=torch.float64, device=dev),
             }
         return self._t
 
@@ -394,7 +395,7 @@ class B200EnvBatch:
         """Episode statistics reduced on device into an f64[8] tensor (NCCL-ready)."""
         t = self._tensors()
         _core.check(self._lib, self._lib.uuvsim_dev_stats(
-            self._handle, t["stats"].data_ptr(), 8, int(clear), self._stream(stream)))
+            self._handle, t["stats"].data_ptr(), len(STAT_NAMES), int(clear), self._stream(stream)))
         return t["stats"]
 
     def capture_graph(self, actions, n_steps: int = 1):

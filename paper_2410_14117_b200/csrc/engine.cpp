@@ -347,6 +347,17 @@ void Engine::parse(const std::string& text) {
             else if (s == "mapped") host_io_ = 1;
             else throw ConfigError("device.host_io must be \"auto\", \"copy\" or \"mapped\"");
         }
+        if (const json* v = opt(*d, "band64")) {
+            if (!v->is_boolean()) throw ConfigError("device.band64 must be a bool");
+            band64_ = v->get<bool>();
+        }
+        if (const json* v = opt(*d, "band_margin")) band_margin_ = num(*v, "device.band_margin");
+        if (const json* v = opt(*d, "band_stream")) {   // "side" (concurrent) | "same" (A/B)
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "side") band_same_ = false;
+            else if (s == "same") band_same_ = true;
+            else throw ConfigError("device.band_stream must be \"side\" or \"same\"");
+        }
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "dense") force_dense_ = true;
@@ -371,70 +382,74 @@ void Engine::parse(const std::string& text) {
 template <> EngineP<float>& Engine::P<float>() { return *pf_; }
 template <> EngineP<double>& Engine::P<double>() { return *pd_; }
 
+// One base vehicle in precision T (engine.rs:234-286 / vehicle.py:64-112 in fp64,
+// then rounded): M_total, its Cholesky factor, the Fossen-pattern dt M^-1, damping,
+// restoring terms, allocation columns and the fp64 originals for DR redraws.
+template <class T> void Engine::fill_vehicle(const BaseVehicle& v, VehP<T>& V) const {
+    std::memset(&V, 0, sizeof(V));
+    double m_rb[36], m_total[36], L[36];
+    mass_matrices(v, m_rb, m_total);
+    if (!cholesky6(m_total, L))
+        throw ConfigError("M_RB + M_A is not positive definite: matrix is not positive definite");
+    for (int k = 0; k < 36; ++k) {
+        V.mtot[k] = (T)m_total[k];
+        V.mrb[k] = (T)m_rb[k];
+        V.ma[k] = (T)v.added[k];
+        V.chol[k] = (T)L[k];
+        V.dlin[k] = (T)v.dlin[k];
+        V.mrb64[k] = m_rb[k];
+        V.ma64[k] = v.added[k];
+    }
+    for (int i = 0; i < 6; ++i) {
+        V.chol_inv[i] = (T)(1.0 / L[i * 6 + i]);
+        V.dquad[i] = (T)v.dquad[i];
+    }
+    {   // sub_dt * M_total^-1 on the Fossen pattern (2x2 blocks {0,4}, {1,3}; 2; 5),
+        // in fp64 from the fp64 matrix, then rounded (fp32 product kernel)
+        const double dt = (double)(T)(task_.control_dt / (double)task_.n_substeps);
+        const int blk[2][2] = {{0, 4}, {1, 3}};
+        for (const auto& bk : blk) {
+            const int i = bk[0], j = bk[1];
+            const double a = m_total[i * 6 + i], b = m_total[i * 6 + j];
+            const double c = m_total[j * 6 + i], d = m_total[j * 6 + j];
+            const double id = dt / (a * d - b * c);
+            V.kdt[i * 6 + i] = (T)(d * id);
+            V.kdt[i * 6 + j] = (T)(-b * id);
+            V.kdt[j * 6 + i] = (T)(-c * id);
+            V.kdt[j * 6 + j] = (T)(a * id);
+        }
+        V.kdt[2 * 6 + 2] = (T)(dt / m_total[2 * 6 + 2]);
+        V.kdt[5 * 6 + 5] = (T)(dt / m_total[5 * 6 + 5]);
+    }
+    V.weight = (T)v.weight;
+    V.buoyancy = (T)v.buoyancy;
+    for (int k = 0; k < 3; ++k) {
+        V.rg[k] = (T)v.rg[k];
+        V.rb[k] = (T)v.rb[k];
+        V.rb64[k] = v.rb[k];
+    }
+    V.weight64 = v.weight;
+    V.wb = (T)(v.weight - v.buoyancy);
+    for (int k = 0; k < 3; ++k) V.hm[k] = (T)(v.weight * v.rg[k] - v.buoyancy * v.rb[k]);
+    const int n = (int)v.kmax.size();
+    V.n_thr = n;
+    for (int i = 0; i < n; ++i) {   // thrusters.py:81-94 / engine.rs:260-271
+        const double px = v.pos[i][0], py = v.pos[i][1], pz = v.pos[i][2];
+        const double dx = v.dir[i][0], dy = v.dir[i][1], dz = v.dir[i][2];
+        V.alloc[0 * MAX_THR + i] = (T)dx;
+        V.alloc[1 * MAX_THR + i] = (T)dy;
+        V.alloc[2 * MAX_THR + i] = (T)dz;
+        V.alloc[3 * MAX_THR + i] = (T)(py * dz - pz * dy);
+        V.alloc[4 * MAX_THR + i] = (T)(pz * dx - px * dz);
+        V.alloc[5 * MAX_THR + i] = (T)(px * dy - py * dx);
+        V.kmax[i] = (T)v.kmax[i];
+        V.curve[i] = v.curve[i];
+    }
+}
+
 template <class T> void Engine::fill_params(EngineP<T>& p) {
     std::memset(&p, 0, sizeof(p));
-    for (size_t vi = 0; vi < veh_.size(); ++vi) {
-        const BaseVehicle& v = veh_[vi];
-        VehP<T>& V = p.veh[vi];
-        double m_rb[36], m_total[36], L[36];
-        mass_matrices(v, m_rb, m_total);
-        if (!cholesky6(m_total, L))
-            throw ConfigError("M_RB + M_A is not positive definite: matrix is not positive definite");
-        for (int k = 0; k < 36; ++k) {
-            V.mtot[k] = (T)m_total[k];
-            V.mrb[k] = (T)m_rb[k];
-            V.ma[k] = (T)v.added[k];
-            V.chol[k] = (T)L[k];
-            V.dlin[k] = (T)v.dlin[k];
-            V.mrb64[k] = m_rb[k];
-            V.ma64[k] = v.added[k];
-        }
-        for (int i = 0; i < 6; ++i) {
-            V.chol_inv[i] = (T)(1.0 / L[i * 6 + i]);
-            V.dquad[i] = (T)v.dquad[i];
-        }
-        {   // sub_dt * M_total^-1 on the Fossen pattern (2x2 blocks {0,4}, {1,3}; 2; 5),
-            // in fp64 from the fp64 matrix, then rounded (fp32 product kernel)
-            const double dt = (double)(T)(task_.control_dt / (double)task_.n_substeps);
-            const int blk[2][2] = {{0, 4}, {1, 3}};
-            for (const auto& bk : blk) {
-                const int i = bk[0], j = bk[1];
-                const double a = m_total[i * 6 + i], b = m_total[i * 6 + j];
-                const double c = m_total[j * 6 + i], d = m_total[j * 6 + j];
-                const double id = dt / (a * d - b * c);
-                V.kdt[i * 6 + i] = (T)(d * id);
-                V.kdt[i * 6 + j] = (T)(-b * id);
-                V.kdt[j * 6 + i] = (T)(-c * id);
-                V.kdt[j * 6 + j] = (T)(a * id);
-            }
-            V.kdt[2 * 6 + 2] = (T)(dt / m_total[2 * 6 + 2]);
-            V.kdt[5 * 6 + 5] = (T)(dt / m_total[5 * 6 + 5]);
-        }
-        V.weight = (T)v.weight;
-        V.buoyancy = (T)v.buoyancy;
-        for (int k = 0; k < 3; ++k) {
-            V.rg[k] = (T)v.rg[k];
-            V.rb[k] = (T)v.rb[k];
-            V.rb64[k] = v.rb[k];
-        }
-        V.weight64 = v.weight;
-        V.wb = (T)(v.weight - v.buoyancy);
-        for (int k = 0; k < 3; ++k) V.hm[k] = (T)(v.weight * v.rg[k] - v.buoyancy * v.rb[k]);
-        const int n = (int)v.kmax.size();
-        V.n_thr = n;
-        for (int i = 0; i < n; ++i) {   // thrusters.py:81-94 / engine.rs:260-271
-            const double px = v.pos[i][0], py = v.pos[i][1], pz = v.pos[i][2];
-            const double dx = v.dir[i][0], dy = v.dir[i][1], dz = v.dir[i][2];
-            V.alloc[0 * MAX_THR + i] = (T)dx;
-            V.alloc[1 * MAX_THR + i] = (T)dy;
-            V.alloc[2 * MAX_THR + i] = (T)dz;
-            V.alloc[3 * MAX_THR + i] = (T)(py * dz - pz * dy);
-            V.alloc[4 * MAX_THR + i] = (T)(pz * dx - px * dz);
-            V.alloc[5 * MAX_THR + i] = (T)(px * dy - py * dx);
-            V.kmax[i] = (T)v.kmax[i];
-            V.curve[i] = v.curve[i];
-        }
-    }
+    for (size_t vi = 0; vi < veh_.size(); ++vi) fill_vehicle(veh_[vi], p.veh[vi]);
     TaskP<T>& tk = p.task;
     for (int k = 0; k < 6; ++k) tk.target[k] = (T)task_.target[k];
     tk.sub_dt = (T)(task_.control_dt / (double)task_.n_substeps);
@@ -477,6 +492,23 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.final_obs = nullptr;
     p.done_f32 = nullptr;
     p.io_f64 = fp64_ ? 1 : 0;   // device face: engine precision; host ABI: set per launch
+    p.veh64 = veh64_.empty() ? nullptr : veh64_.data();
+    p.sub_dt64 = task_.control_dt / (double)task_.n_substeps;
+    p.veh64_dev = d_veh64_;
+    p.band_theta = band_grid_ > 0 ? BAND_THETA : INFINITY;
+    p.band_kdt = (float)task_.control_dt;
+    p.band_margin = (float)(band_margin_ >= -1e30 ? band_margin_
+                                                   : 0.01 + 8.0 * task_.control_dt * task_.control_dt);
+    p.band_per = band_per_;
+    p.band_grid = band_grid_;
+    p.stats_band = stats_part_ + (size_t)nblk_ * NSTAT;
+    p.band_ctr = reinterpret_cast<unsigned long long*>(d_band_f_);   // 2 counters, then the flags
+    p.band_f = d_band_f_ ? d_band_f_ + 64 : nullptr;
+    p.band_inv_n = 1.0 / (double)m_;
+    p.band_side = band_same_ ? nullptr : band_side_;
+    p.band_same = band_same_ ? 1 : 0;
+    p.band_ev[0] = band_ev_[0];
+    p.band_ev[1] = band_ev_[1];
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are
     // already three 128-bit stores per env (measured)
     const bool stage_ok = obs_dim_ <= MAX_STAGE_DIM;
@@ -503,6 +535,8 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
         p.dr0 = (V4<T>*)carve(N * sizeof(V4<T>));
         p.dr1 = (V4<T>*)carve(N * sizeof(V4<T>));
         p.dr2 = (V2<T>*)carve(N * sizeof(V2<T>));
+        // the exact fp64 record beside the fp32 one, read only by the band replay
+        if (!fp64_ && band64_) p.dr64 = (V2<double>*)carve(N * 5 * sizeof(V2<double>));
     }
     if (off > arena_bytes_) throw RuntimeError("internal: arena too small");
     arena_used_ = off;
@@ -542,6 +576,7 @@ void Engine::allocate() {
     const size_t sT = fp64_ ? 8 : 4;
     size_t bytes = 3 * align256(N * 4 * sT) + 2 * align256(N * 4) + 2 * align256(N * 8) + 256;
     if (ranges_.enabled) bytes += 2 * align256(N * 4 * sT) + align256(N * 2 * sT);
+    if (ranges_.enabled && !fp64_ && band64_) bytes += align256(N * 80);
     size_t free_b = 0, total_b = 0;
     cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     // the host-ABI staging buffers are allocated on first use (ensure_staging):
@@ -553,8 +588,31 @@ void Engine::allocate() {
     cuda_check(cudaMalloc(&arena_, bytes), "cudaMalloc(state)");
     cuda_check(cudaMemset(arena_, 0, bytes), "cudaMemset(state)");
     nblk_ = (int)((m_ + BLOCK - 1) / BLOCK);
-    cuda_check(cudaMalloc(&stats_part_, (size_t)nblk_ * NSTAT * sizeof(double)), "cudaMalloc(stats)");
-    cuda_check(cudaMemset(stats_part_, 0, (size_t)nblk_ * NSTAT * sizeof(double)), "cudaMemset(stats)");
+    // per-block statistics partials: the step kernel's blocks, then the band
+    // replay kernel's (fp32 engines with band64)
+    // band kernel: chunks of n/64 envs (2,048-16,384, a multiple of 2,048): about
+    // one pass of candidates per block, few long-lived blocks beside the step
+    if (!fp64_ && band64_) {
+        const int64_t per = std::min<int64_t>(16384, std::max<int64_t>(2048, (m_ / 64 + 2047) / 2048 * 2048));
+        band_per_ = (int)per;
+        band_grid_ = (int)std::min<int64_t>(65536, (m_ + per - 1) / per);
+    }
+    // per-block statistics partials: the step kernel's blocks, then the band kernel's
+    nstat_blk_ = nblk_ + band_grid_;
+    cuda_check(cudaMalloc(&stats_part_, (size_t)nstat_blk_ * NSTAT * sizeof(double)), "cudaMalloc(stats)");
+    cuda_check(cudaMemset(stats_part_, 0, (size_t)nstat_blk_ * NSTAT * sizeof(double)), "cudaMemset(stats)");
+    if (band_grid_ > 0) {
+        cuda_check(cudaMalloc(&d_band_f_, (size_t)m_ * 4 + 256), "cudaMalloc(band flags)");
+        cuda_check(cudaMemset(d_band_f_, 0, (size_t)m_ * 4 + 256), "cudaMemset(band flags)");
+        // highest priority: as step-kernel blocks retire, the band kernel's small
+        // blocks take the freed room before the step kernel's next wave
+        int lo = 0, hi = 0;
+        cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+        cuda_check(cudaStreamCreateWithPriority(&band_side_, cudaStreamNonBlocking, hi),
+                   "cudaStreamCreate(band)");
+        for (auto& ev : band_ev_)
+            cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate(band)");
+    }
     cuda_check(cudaMalloc(&d_stats_out_, NSTAT * sizeof(double)), "cudaMalloc(stats_out)");
     if (task_.kind != 0) {   // reference trajectory by step index (task.rs:67-74)
         const int64_t len = task_.episode_len + task_.lookahead + 1;
@@ -667,6 +725,13 @@ Engine::Engine(const std::string& text) {
     pair_ = pair_ok && (pair_mode_ == 1 || (pair_mode_ < 0 && m_ >= PAIR_AUTO_MIN_ENVS));
     try {
         allocate();
+        if (!fp64_) {   // fp64 base vehicles: band-kernel parameters and step-kernel tail
+            veh64_.assign(MAX_VEH, VehP<double>{});
+            for (size_t vi = 0; vi < veh_.size(); ++vi) fill_vehicle(veh_[vi], veh64_[vi]);
+            cuda_check(cudaMalloc(&d_veh64_, MAX_VEH * sizeof(VehP<double>)), "cudaMalloc(veh64)");
+            cuda_check(cudaMemcpy(d_veh64_, veh64_.data(), MAX_VEH * sizeof(VehP<double>),
+                                  cudaMemcpyHostToDevice), "veh64");
+        }
         if (fp64_) {
             pd_ = std::make_unique<EngineP<double>>();
             fill_params(*pd_);
@@ -692,9 +757,18 @@ void Engine::release() {
         g = AbiGraph{};
     }
     free_staging();
-    void* bufs[] = {arena_, traj_, stats_part_, d_pack_, d_flag_, d_stats_out_, d_vpack_};
+    void* bufs[] = {arena_, traj_, stats_part_, d_pack_, d_flag_, d_stats_out_, d_vpack_, d_veh64_,
+                    d_band_f_};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    d_veh64_ = nullptr;
+    d_band_f_ = nullptr;
+    if (band_side_) cudaStreamDestroy(band_side_);
+    band_side_ = nullptr;
+    for (auto& ev : band_ev_) {
+        if (ev) cudaEventDestroy(ev);
+        ev = nullptr;
+    }
     arena_ = traj_ = nullptr;
     stats_part_ = d_pack_ = d_stats_out_ = nullptr;
     d_flag_ = nullptr;
@@ -1066,13 +1140,19 @@ void Engine::restore(const void* in, size_t len) {
     cuda_check(cudaDeviceSynchronize(), "restore sync");
     cuda_check(cudaMemcpy(arena_, static_cast<const char*>(in) + sizeof(h), arena_used_,
                           cudaMemcpyHostToDevice), "restore H2D");
-    if (fp64_) pd_->seed = h.root_seed;
-    else pf_->seed = h.root_seed;
+    if (fp64_) {
+        pd_->seed = h.root_seed;
+    } else {
+        pf_->seed = h.root_seed;
+        // band flags follow the restored states
+        cuda_check(Launch<float>::band_flags(*pf_, stream_), "band flags");
+        cuda_check(cudaStreamSynchronize(stream_), "restore sync");
+    }
 }
 
 void Engine::stats_host(double* out, bool clear) {
     activate();
-    cuda_check(launch_stats_reduce(stats_part_, nblk_, d_stats_out_, clear ? 1 : 0, stream_), "stats");
+    cuda_check(launch_stats_reduce(stats_part_, nstat_blk_, d_stats_out_, clear ? 1 : 0, stream_), "stats");
     cuda_check(cudaMemcpyAsync(out, d_stats_out_, NSTAT * 8, cudaMemcpyDeviceToHost, stream_), "stats D2H");
     cuda_check(cudaStreamSynchronize(stream_), "stats sync");
 }
@@ -1158,7 +1238,7 @@ void Engine::dev_bench_actions(void* act, cudaStream_t st) {
 
 void Engine::dev_stats(double* out, bool clear, cudaStream_t st) {
     check_device();
-    cuda_check(launch_stats_reduce(stats_part_, nblk_, out, clear ? 1 : 0, st), "dev_stats");
+    cuda_check(launch_stats_reduce(stats_part_, nstat_blk_, out, clear ? 1 : 0, st), "dev_stats");
 }
 
 void Engine::graph_capture(const void* act, void* obs, void* rew, uint8_t* done,
@@ -1217,6 +1297,7 @@ std::string Engine::info() const {
         {"pattern", fossen_ ? "fossen" : "dense"},
         {"envs_per_thread", pair_ ? 2 : 1},
         {"tma_pipelined", (fp64_ ? 0 : pf_->persist_blocks) > 0},
+        {"band64", !fp64_ && band64_},
         {"stage_obs", (fp64_ ? pd_->stage_obs : pf_->stage_obs) != 0},
         {"host_io", host_io_ == 0 ? "copy" : host_io_ == 1 ? "mapped" : "auto"},
         {"arena_address", (uint64_t)(uintptr_t)arena_},

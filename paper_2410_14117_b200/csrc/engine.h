@@ -122,6 +122,7 @@ private:
     void init_randomization();
     template <class T> EngineP<T>& P();
     template <class T> void fill_params(EngineP<T>& p);
+    template <class T> void fill_vehicle(const BaseVehicle& v, VehP<T>& V) const;
     template <class T> void step_host_T(const double* act, double* obs, double* rew,
                                         uint8_t* done, int8_t* reason);
     template <class T> void reset_host_T(uint64_t seed, double* obs);
@@ -136,6 +137,9 @@ private:
     bool stats_on_ = true;
     bool fossen_ = false;
     bool force_dense_ = false;
+    bool band64_ = true;      // device.band64: fp64 recompute of steps entering the pitch band
+    bool band_same_ = false;
+    double band_margin_ = -1e300;   // device.band_margin override (experiments; default by control_dt)  // device.band_stream "same": band kernel after the step, one stream
     int pair_mode_ = -1;      // device.pair: -1 auto, 0 off, 1 on
     int stage_mode_ = -1;     // device.stage_obs: -1 auto, 0 off, 1 on
     int tma_mode_ = -1;       // device.tma: -1 auto, 0 off, 1 on
@@ -159,6 +163,13 @@ private:
     void* traj_ = nullptr;
     double* stats_part_ = nullptr;
     int nblk_ = 0;
+    int band_grid_ = 0;       // blocks of the band kernel (0: band64 off)
+    int band_per_ = 0;        // envs scanned per band-kernel block
+    int nstat_blk_ = 0;       // stats partial slots: step blocks + band blocks
+    VehP<double>* d_veh64_ = nullptr;        // fp64 base vehicles (step-kernel tail)
+    uint32_t* d_band_f_ = nullptr;           // band generation (2 words) + per-env flags
+    cudaStream_t band_side_ = nullptr;       // band kernel stream (fork / join per step)
+    cudaEvent_t band_ev_[2] = {nullptr, nullptr};
     // ABI staging (f64 host layout; fp32 engines convert on device)
     void* d_actT_ = nullptr;
     void* d_obsT_ = nullptr;
@@ -172,6 +183,7 @@ private:
     int* d_flag_ = nullptr;
     double* d_stats_out_ = nullptr;
     float4* d_vpack_ = nullptr;
+    std::vector<VehP<double>> veh64_;   // fp64 base vehicles (band replay parameters)
     cudaStream_t stream_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     // host-ABI step replayed as one CUDA graph (H2D -> step -> D2H) while the

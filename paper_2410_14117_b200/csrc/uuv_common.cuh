@@ -31,7 +31,7 @@ namespace uuv {
 
 constexpr int MAX_THR = 8;
 constexpr int MAX_VEH = 2;
-constexpr int NSTAT = 8;
+constexpr int NSTAT = 9;
 
 // stats slots (per-block partial sums, reduced on read)
 enum StatSlot {
@@ -43,7 +43,14 @@ enum StatSlot {
     ST_EP_LEN = 5,       // sum of lengths of completed episodes
     ST_STEPS = 6,        // env-steps executed
     ST_RESAMPLE_ERR = 7, // per-episode DR resamples rejected (non-PD), params kept
+    ST_BAND64 = 8,       // fp32-engine env-steps computed in fp64 (Euler pitch band)
 };
+
+// Euler-singularity band: near theta = +-pi/2 the Euler-rate map's
+// 1/cos(theta) turns fp32 rounding of the state into errors far beyond the fp32
+// tolerance, so a step that starts at |theta| <= BAND_THETA and may leave it is
+// computed in fp64 (uuv_kernels.cuh band_cand / replay_band64).
+constexpr float BAND_THETA = 1.4f;
 
 template <class T> struct alignas(4 * sizeof(T)) V4 { T x, y, z, w; };
 template <class T> struct alignas(2 * sizeof(T)) V2 { T x, y; };
@@ -203,6 +210,35 @@ template <class T> struct EngineP {
     float* done_f32;
     int32_t stage_act;     // host-ABI zero-copy step: f64 action rows staged in shared memory
     int32_t stagger_ns;    // host-ABI zero-copy step: block b starts b*stagger_ns/gridDim ns late
+    // fp64 band replay (fp32 engines; see uuv_kernels.cuh band_cand):
+    // veh64 = fp64 base vehicles in HOST memory (copied into the band kernel's
+    // parameters at launch), veh64_dev = the same in device memory (step-kernel
+    // tail); band_theta = BAND_THETA, or +inf with device.band64 = false
+    const VehP<double>* veh64;
+    const VehP<double>* veh64_dev;
+    V2<double>* dr64;      // [N][5] exact fp64 DR records (randomised fp32 engines)
+    double sub_dt64;
+    float band_theta;
+    float band_kdt;        // candidate predictor: control_dt
+    float band_margin;     // candidate predictor margin (rad)
+    int32_t band_per;      // envs scanned per band-kernel block (multiple of BLOCK)
+    int32_t band_grid;     // band-kernel blocks
+    int32_t band_same;     // band kernel on the launching stream after the step (A/B only)
+    double* stats_band;    // the band kernel's per-block statistics partials
+    // Band ownership per env and step (uuv_kernels.cuh k_band): flag word
+    // band_f[e] = generation << 1 | candidate, written by whichever kernel steps
+    // the env for the next step.  The step kernel steps env e iff band_f[e] ==
+    // gen << 1, the band kernel iff == gen << 1 | 1.  Each kernel derives gen from
+    // its own env counter (band_ctr[0] step kernel, [1] band kernel): every block
+    // adds its env count at its end, so a block reading the counter at its start
+    // sees k * n_env + (less than n_env) during step k -> gen = counter / n_env.
+    uint32_t* band_f;
+    unsigned long long* band_ctr;
+    double band_inv_n;     // 1 / n_env
+    // host-only: the band kernel runs on band_side, forked from / joined to the
+    // launching stream through these events (cudaStream_t / cudaEvent_t)
+    void* band_side;
+    void* band_ev[2];
 };
 
 constexpr int PACK_F4 = 10;   // 40 floats: Fossen pattern + restoring + trig constants

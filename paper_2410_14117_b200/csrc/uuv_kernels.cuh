@@ -15,6 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#ifdef UUV_BAND_CLOCK
+#include <cstdio>
+#endif
 
 #include <algorithm>
 #include <type_traits>
@@ -78,11 +81,124 @@ __device__ __forceinline__ void replay_env(const EngineP<float>& p, const VehP<f
     }
 }
 
+// fp64 step of one env (the Euler pitch band): near theta = +-pi/2
+// the Euler-rate map (tan, sec of theta) amplifies the fp32 rounding of the state
+// by up to 1/cos(PITCH_LIMIT) = 1000, beyond the fp32 tolerance, so a step that
+// may leave |theta| <= band_theta runs in fp64 from the step-initial fp32 state:
+// the FMA formulation of substep_fused in fp64 for the Fossen pattern (the
+// reference's operation order, substep_ref, otherwise), fp64 vehicle constants and
+// -- under domain randomisation -- the env's exact fp64 record (randomize.py:79-109).
+// Returns the state rounded to fp32 by value.  Used by the band kernel (k_band)
+// for predicted candidates and by the step kernel's out-of-line tail (band_tail)
+// for predictor misses.
+struct Band64Out {
+    float v[12];
+    int failed;
+};
+
+template <bool DR, class Pat>
+__device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, const VehP<double>& V,
+                                                   const float s32[12], const V2<double> rec[5],
+                                                   const double act[MAX_THR]) {
+    double s[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) s[i] = s32[i];
+    if (!(fmax(fabs(s[3]), fmax(fabs(s[4]), fabs(s[5]))) <= 3.141592653589793)) {
+        s[3] = wrap_pi64(s[3]);   // teacher-forced out-of-range angles (sincos64's range)
+        s[4] = wrap_pi64(s[4]);
+        s[5] = wrap_pi64(s[5]);
+    }
+    const double dt = p.sub_dt64;
+    EnvParams<double, DR> E;
+    if constexpr (DR) {   // the env's exact fp64 record (written with its fp32 twin)
+        build_env<double, Pat>(V, V4<double>{rec[0].x, rec[0].y, rec[1].x, rec[1].y},
+                               V4<double>{rec[2].x, rec[2].y, rec[3].x, rec[3].y},
+                               V2<double>{rec[4].x, rec[4].y}, dt, E);
+        if constexpr (Pat::fossen) fossen_kdt<double>(E.mtot, dt, E.kdt);
+    }
+    double tau[6];
+    wrench<double, DR, DR>(V, E, act, true, tau);
+    Band64Out o;
+    o.failed = 0;
+    // failure = a component non-finite or outside the fp32 range: the fp32
+    // engine's own failure criterion (model.rs:186-193 with an fp32 state).  The
+    // Fossen path runs every sub-step unchecked and tests the final state; only
+    // a failed step is re-run from the start with a check after each sub-step
+    // (keeping the last good state), like the fp32 kernel's replay_env.
+    bool checked = !Pat::fossen;
+    if constexpr (Pat::fossen) {
+        double t[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) t[i] = s[i];
+#pragma unroll 1
+        for (int k = 0; k < p.task.n_substeps; ++k) substep_f64<DR, false>(V, E, t, tau, dt);
+        if (f32_range12(t)) {
+#pragma unroll
+            for (int i = 0; i < 12; ++i) s[i] = t[i];
+        } else {
+            checked = true;
+        }
+    }
+    if (checked) {
+#pragma unroll 1
+        for (int k = 0; k < p.task.n_substeps; ++k) {
+            bool ok;
+            if constexpr (Pat::fossen) {
+                ok = substep_f64<DR, true>(V, E, s, tau, dt);
+            } else {
+                double t[12];
+#pragma unroll
+                for (int i = 0; i < 12; ++i) t[i] = s[i];
+                ok = substep<double, DR, Pat>(V, E, t, tau, dt) && f32_range12(t);
+                if (ok) {
+#pragma unroll
+                    for (int i = 0; i < 12; ++i) s[i] = t[i];
+                }
+            }
+            if (!ok) {
+                o.failed = 1;
+                break;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) o.v[i] = (float)s[i];
+    return o;
+}
+
 // Per-thread episode-statistics accumulator (one or two envs per thread).
 struct StatAcc {
     float rew = 0.f, epret = 0.f;
-    int eplen = 0, n_tr = 0, n_dv = 0, n_fl = 0, n_act = 0, n_err = 0;
+    int eplen = 0, n_tr = 0, n_dv = 0, n_fl = 0, n_act = 0, n_err = 0, n_b64 = 0;
 };
+
+// Band candidates: envs inside |theta| <= band_theta whose pitch could leave it
+// within this control step -- moving toward the band edge at the current pitch
+// rate theta_dot = cos(phi) q - sin(phi) r (dynamics.py:279-282):
+//   |theta| + control_dt max(0, sign(theta) theta_dot) + margin > band_theta,
+// margin = 0.01 + 8 control_dt^2 rad for the pitch acceleration over the step
+// (calibrated on the oracle under bench actions: the largest margin an actual
+// band exit needed was 0.0033 rad at control_dt = 0.05 s, tools/band_calibrate.py).
+// The decision is stored with the state (EngineP::band_f), so the step kernel and
+// the band kernel read the same bit; a miss is still computed in fp64
+// (band_tail), only later.
+__device__ __forceinline__ bool band_cand(const EngineP<float>& p, const float s[12]) {
+    const float a = fabsf(s[4]);
+    if (!(a <= p.band_theta)) return false;
+    // |theta_dot| <= |q| + |r|: most envs are decided here, without sin / cos
+    if (a + p.band_kdt * (fabsf(s[10]) + fabsf(s[11])) + p.band_margin <= p.band_theta) return false;
+    float sphi, cphi;
+    sincos_t(s[3], &sphi, &cphi);
+    const float td = copysignf(1.0f, s[4]) * fmaf(cphi, s[10], -sphi * s[11]);
+    return a + p.band_kdt * fmaxf(td, 0.0f) + p.band_margin > p.band_theta;
+}
+
+// A non-candidate whose fp32 pitch trajectory still left the band (a predictor
+// miss; p.s1[e].x is the step-initial theta, still in HBM): finished from an
+// fp64 recompute at the end of the step kernel (band_tail)
+__device__ __forceinline__ bool band_exit(const EngineP<float>& p, int e, float thmax) {
+    return thmax > p.band_theta && fabsf(p.s1[e].x) <= p.band_theta;
+}
 
 // Reward / termination / auto-reset / stores / observation for one env whose
 // sub-steps are done (tasks.py:219-230, batch.py:101-118, engine.rs:543-568).
@@ -101,11 +217,23 @@ constexpr int LA_PRE = 5;
 // them in local memory -- an STL that waits for the loads before the first
 // sub-step, then LDLs -- so there the prologue only prefetches their cache
 // lines into L1 and finish_env reads the table (L1 hits).
+// this step's band generation from a kernel's env counter (EngineP::band_ctr)
+template <class T>
+__device__ __forceinline__ uint32_t band_gen(const EngineP<T>& p, unsigned long long c) {
+    unsigned long long k = (unsigned long long)floor((double)c * p.band_inv_n);
+    const unsigned long long n = (unsigned long long)p.n_env;
+    if (k * n > c) --k;
+    else if ((k + 1) * n <= c) ++k;
+    return (uint32_t)k & 0x7fffffffu;
+}
+
 template <class T, bool TRACK, bool RR = TRACK> struct EnvIn {
     static constexpr bool kRegRows = TRACK && RR;
     T s[12];
     int32_t step;
     float ep_ret;
+    uint32_t bf = 0;   // band flag word (fp32 engines with band64): generation << 1 | candidate
+    uint32_t bk = 0;   // this step's generation (band_gen)
     V4<T> rows[kRegRows ? LA_PRE + 1 : 1];   // traj[step+1 .. step+1+LA_PRE]
 };
 
@@ -117,6 +245,7 @@ __device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TR
     in.s[8] = a2.x; in.s[9] = a2.y; in.s[10] = a2.z; in.s[11] = a2.w;
     in.step = p.step[e];
     in.ep_ret = p.ep_ret[e];
+    if (p.band_f) in.bf = p.band_f[e];
     if constexpr (TRACK) {
         const int tab_last = p.task.episode_len + p.task.lookahead;
         if constexpr (EnvIn<T, TRACK, RR>::kRegRows) {
@@ -240,7 +369,8 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
                 uint64_t pc = p.param_ctr[e];
                 V4<T> n0, n1;
                 V2<T> n2;
-                if (dr_draw<T, Pat>(V, p.ranges, seed, g, pc, n0, n1, n2)) {
+                if (dr_draw<T, Pat>(V, p.ranges, seed, g, pc, n0, n1, n2,
+                                    p.dr64 ? p.dr64 + (size_t)e * 5 : nullptr)) {
                     p.dr0[e] = n0; p.dr1[e] = n1; p.dr2[e] = n2;
                 } else {
                     st.n_err += 1;
@@ -257,6 +387,11 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     }
     p.ep_ret[e] = er;
     p.step[e] = nstep;
+    if constexpr (!is_f64<T>()) {   // next step's band decision, one generation on
+        if (p.band_f)
+            p.band_f[e] = (((in.bk + 1u) & 0x7fffffffu) << 1) |
+                          (band_cand(p, s) ? 1u : 0u);
+    }
     p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
     p.s1[e] = V4<T>{s[4], s[5], s[6], s[7]};
     p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
@@ -267,11 +402,12 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     // contiguously afterwards (flush_obs); else straight to HBM
     const size_t D = (size_t)tk.obs_dim;
     if (p.io_f64) {
-        double* row = p.stage_obs ? (double*)uuv_smem + (size_t)li * D : (double*)obs + (size_t)e * D;
+        double* row = (p.stage_obs && li >= 0) ? (double*)uuv_smem + (size_t)li * D
+                                               : (double*)obs + (size_t)e * D;
         write_obs<T, double, TRACK>(tk, row, s, in, nstep, pre);
         ((double*)rew)[e] = (double)reward;
     } else {
-        T* row = p.stage_obs ? (T*)uuv_smem + (size_t)li * D : (T*)obs + (size_t)e * D;
+        T* row = (p.stage_obs && li >= 0) ? (T*)uuv_smem + (size_t)li * D : (T*)obs + (size_t)e * D;
         write_obs<T, T, TRACK>(tk, row, s, in, nstep, pre);
         ((T*)rew)[e] = reward;
     }
@@ -300,17 +436,27 @@ __device__ __forceinline__ void load_state(const EngineP<T>& p, int e, T s[12]) 
     s[8] = a2.x; s[9] = a2.y; s[10] = a2.z; s[11] = a2.w;
 }
 
+// Outcome of one env in the step kernel: finished here, left to the concurrent
+// band kernel (candidate), or left to this kernel's fp64 tail (band_tail).
+enum EnvCode { ENV_DONE = 0, ENV_BAND = 1, ENV_TAIL = 2 };
+
 // One env per thread (every precision / pattern / randomisation mode).
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
-__device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uint64_t g,
-                                         const void* __restrict__ act, void* __restrict__ obs,
-                                         void* __restrict__ rew, uint8_t* __restrict__ done,
-                                         int8_t* __restrict__ reason, StatAcc& st) {
+__device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint64_t g,
+                                        const void* __restrict__ act, void* __restrict__ obs,
+                                        void* __restrict__ rew, uint8_t* __restrict__ done,
+                                        int8_t* __restrict__ reason, StatAcc& st) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
     EnvIn<T, TRACK, !DR> in;
     load_env<T, TRACK>(p, e, in);
     T* s = in.s;
+    // not this kernel's env this step: a band candidate (or already stepped by the
+    // concurrent band kernel)
+    if (p.band_f) {
+        in.bk = band_gen(p, p.band_ctr[0]);
+        if (in.bf != (in.bk << 1)) return ENV_BAND;
+    }
     if constexpr (!is_f64<T>()) prewrap(s);
 
     // fp32: Fossen-pattern parameters in registers (UUV_PACK_CONSTS) or in the
@@ -347,21 +493,27 @@ __device__ __forceinline__ void step_env(const EngineP<T>& p, int e, int li, uin
         // recorded and the env replayed from its initial state (still in HBM)
         // up to the last finite sub-step
         const float dt = dt32;
+        float thm = 0.0f;   // max |theta| over the sub-steps
 #pragma unroll 1
-        for (int k = 0; k < tk.n_substeps; ++k) substep_fused<DR, Pat, false>(V, E, s, tau, dt, K);
+        for (int k = 0; k < tk.n_substeps; ++k) {
+            substep_fused<DR, Pat, false>(V, E, s, tau, dt, K);
+            thm = fmaxf(thm, fabsf(s[4]));
+        }
+        if (band_exit(p, e, thm)) return ENV_TAIL;
         if (!all_finite12(s)) {
             failed = true;
             replay_env<DR, Pat>(p, V, E, e, tau, dt, K, tk.n_substeps, s);
         }
     }
     finish_env<T, TRACK, DR, SLOT, Pat>(p, e, li, g, s, in, failed, obs, rew, done, reason, st);
+    return ENV_DONE;
 }
 
 // Two envs per thread sharing the register-resident vehicle constants (fp32,
 // Fossen pattern, no randomisation): two independent dependency chains per
 // thread hide latency at half the registers of two threads.
 template <bool TRACK, int SLOT>
-__device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e1, int li0,
+__device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1, int li0,
                                           int li1, EnvIn<float, TRACK, false>& in0,
                                           EnvIn<float, TRACK, false>& in1, const void* act0,
                                           const void* act1, bool io_f64, void* __restrict__ obs,
@@ -372,6 +524,9 @@ __device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e
     const TaskP<float>& tk = p.task;
     float* s0 = in0.s;
     float* s1 = in1.s;
+    if (p.band_f) in0.bk = in1.bk = band_gen(p, p.band_ctr[0]);
+    const bool cand0 = p.band_f && in0.bf != (in0.bk << 1);
+    const bool cand1 = p.band_f && in1.bf != (in1.bk << 1);
     prewrap(s0);
     prewrap(s1);
     constexpr bool REG = UUV_PACK_CONSTS;
@@ -386,22 +541,33 @@ __device__ __forceinline__ void pair_core(const EngineP<float>& p, int e0, int e
     float tau0[6], tau1[6];
     wrench<float, false, REG>(V, E, act0, io_f64, tau0);
     wrench<float, false, REG>(V, E, act1, io_f64, tau1);
+    float thm0 = 0.0f, thm1 = 0.0f;   // max |theta| over the sub-steps
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
         substep_fused<false, Pat, false>(V, E, s0, tau0, dt, K);
         substep_fused<false, Pat, false>(V, E, s1, tau1, dt, K);
+        thm0 = fmaxf(thm0, fabsf(s0[4]));
+        thm1 = fmaxf(thm1, fabsf(s1[4]));
     }
-    const bool f0 = !all_finite12(s0), f1 = !all_finite12(s1);
+    // codes: candidates (decided on entry) belong to the band kernel, misses to
+    // the fp64 tail; both computed here anyway (two lockstep chains)
+    const int c0 = cand0 ? ENV_BAND : (band_exit(p, e0, thm0) ? ENV_TAIL : ENV_DONE);
+    const int c1 = cand1 ? ENV_BAND : (band_exit(p, e1, thm1) ? ENV_TAIL : ENV_DONE);
+    const bool f0 = c0 == ENV_DONE && !all_finite12(s0), f1 = c1 == ENV_DONE && !all_finite12(s1);
     if (f0) replay_env<false, Pat>(p, V, E, e0, tau0, dt, K, tk.n_substeps, s0);
     if (f1) replay_env<false, Pat>(p, V, E, e1, tau1, dt, K, tk.n_substeps, s1);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e0, li0, p.env_offset + (uint64_t)e0, s0, in0,
-                                               f0, obs, rew, done, reason, st);
-    finish_env<float, TRACK, false, SLOT, Pat>(p, e1, li1, p.env_offset + (uint64_t)e1, s1, in1,
-                                               f1, obs, rew, done, reason, st);
+    const uint64_t g0 = p.env_offset + (uint64_t)e0, g1 = p.env_offset + (uint64_t)e1;
+    if (c0 == ENV_DONE)
+        finish_env<float, TRACK, false, SLOT, Pat>(p, e0, li0, g0, s0, in0, f0, obs, rew, done,
+                                                   reason, st);
+    if (c1 == ENV_DONE)
+        finish_env<float, TRACK, false, SLOT, Pat>(p, e1, li1, g1, s1, in1, f1, obs, rew, done,
+                                                   reason, st);
+    return c0 | (c1 << 2);
 }
 
 template <bool TRACK, int SLOT>
-__device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e1, int li0,
+__device__ __forceinline__ int step_pair(const EngineP<float>& p, int e0, int e1, int li0,
                                           int li1,
                                           const void* __restrict__ act, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
@@ -409,14 +575,15 @@ __device__ __forceinline__ void step_pair(const EngineP<float>& p, int e0, int e
     EnvIn<float, TRACK, false> in0, in1;
     load_env<float, TRACK>(p, e0, in0);
     load_env<float, TRACK>(p, e1, in1);
-    pair_core<TRACK, SLOT>(p, e0, e1, li0, li1, in0, in1, act_row(p, act, e0),
-                           act_row(p, act, e1), p.io_f64, obs, rew, done, reason, st);
+    return pair_core<TRACK, SLOT>(p, e0, e1, li0, li1, in0, in1, act_row(p, act, e0),
+                                  act_row(p, act, e1), p.io_f64, obs, rew, done, reason, st);
 }
 
 // Block-level episode statistics: warp reductions -> shared memory -> one
 // read-modify-write of this block's own partial slot (no atomics, deterministic).
+template <int NT = BLOCK>
 __device__ __forceinline__ void block_stats(double* __restrict__ part, const StatAcc& st) {
-    __shared__ double sh[BLOCK / 32][NSTAT];
+    __shared__ double sh[NT / 32][NSTAT];
     const unsigned full = 0xffffffffu;
     float r = st.rew, er = st.epret;
 #pragma unroll
@@ -430,6 +597,7 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
     const int n_fl = __reduce_add_sync(full, st.n_fl);
     const int n_ac = __reduce_add_sync(full, st.n_act);
     const int n_er = __reduce_add_sync(full, st.n_err);
+    const int n_b64 = __reduce_add_sync(full, st.n_b64);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) {
         sh[w][ST_REWARD] = r;
@@ -440,12 +608,13 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
         sh[w][ST_EP_LEN] = el;
         sh[w][ST_STEPS] = n_ac;
         sh[w][ST_RESAMPLE_ERR] = n_er;
+        sh[w][ST_BAND64] = n_b64;
     }
     __syncthreads();
     if (threadIdx.x < NSTAT) {
         double acc = 0.0;
 #pragma unroll
-        for (int i = 0; i < BLOCK / 32; ++i) acc += sh[i][threadIdx.x];
+        for (int i = 0; i < NT / 32; ++i) acc += sh[i][threadIdx.x];
         // RED (no return): one update per slot per step, steps are stream-ordered,
         // so the accumulation order -- and the sum -- is deterministic
         atomicAdd(&part[(size_t)blockIdx.x * NSTAT + threadIdx.x], acc);
@@ -453,39 +622,74 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
 }
 
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
-__device__ __forceinline__ void one_env(const EngineP<T>& p, int e, int li, const void* act,
-                                        void* obs, void* rew, uint8_t* done, int8_t* reason,
-                                        StatAcc& st) {
+__device__ __forceinline__ int one_env(const EngineP<T>& p, int e, int li, const void* act,
+                                       void* obs, void* rew, uint8_t* done, int8_t* reason,
+                                       StatAcc& st) {
     const uint64_t g = p.env_offset + (uint64_t)e;
     bool slot1 = false;
     if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
-    if (!slot1)
-        step_env<T, TRACK, DR, 0, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
-    else if constexpr (MIX)
-        step_env<T, TRACK, DR, 1, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+    if (!slot1) return step_env<T, TRACK, DR, 0, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+    if constexpr (MIX)
+        return step_env<T, TRACK, DR, 1, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+    return ENV_DONE;
 }
 
 // Store the block's staged observation rows (envs [first, first+n)) with
 // contiguous 128-bit stores: full 128-B lines instead of one partial sector
-// per env and store instruction.
+// per env and store instruction.  Rows flagged in `skip` (bit per row: envs this
+// kernel did not finish -- band candidates, fp64 tail) are left untouched; rows
+// are a multiple of 8 bytes, so 16-byte chunks (rows of 16k bytes) or 8-byte
+// chunks never straddle a skipped and a kept row.
+template <class C>
+__device__ __forceinline__ void copy_rows(unsigned char* __restrict__ dst, size_t nbytes,
+                                          uint32_t row_bytes, const uint32_t* skip) {
+    const C* src = reinterpret_cast<const C*>(uuv_smem);
+    C* d = reinterpret_cast<C*>(dst);
+    const size_t n = nbytes / sizeof(C);
+    if (!skip) {
+        for (size_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
+        return;
+    }
+    // row of chunk i, tracked incrementally (one division per thread)
+    const uint32_t step_b = blockDim.x * (uint32_t)sizeof(C);
+    const uint32_t drow = step_b / row_bytes, doff = step_b % row_bytes;
+    uint32_t row = threadIdx.x * (uint32_t)sizeof(C) / row_bytes;
+    uint32_t off = threadIdx.x * (uint32_t)sizeof(C) % row_bytes;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if (!((skip[row >> 5] >> (row & 31)) & 1u)) d[i] = src[i];
+        row += drow;
+        off += doff;
+        if (off >= row_bytes) {
+            off -= row_bytes;
+            ++row;
+        }
+    }
+}
+
 template <class T>
 __device__ __forceinline__ void flush_obs(const EngineP<T>& p, void* __restrict__ obs, int first,
-                                          int n) {
+                                          int n, const uint32_t* skip_mask = nullptr) {
     __syncthreads();
     if (n <= 0) return;
     const size_t D = (size_t)p.task.obs_dim;
     const size_t nel = (size_t)n * D;
     const size_t esz = p.io_f64 ? 8 : sizeof(T);
     const size_t nbytes = nel * esz;
+    const uint32_t rb = (uint32_t)(D * esz);
     unsigned char* dst = (unsigned char*)obs + (size_t)first * D * esz;
-    if (((uintptr_t)dst & 15) == 0 && (nbytes & 15) == 0) {
-        const float4* s4 = reinterpret_cast<const float4*>(uuv_smem);
-        float4* d4 = reinterpret_cast<float4*>(dst);
-        for (size_t i = threadIdx.x; i < nbytes / 16; i += blockDim.x) d4[i] = s4[i];
+    // any row to skip in this block?
+    const uint32_t* skip = nullptr;
+    if (skip_mask) {
+        uint32_t any = 0;
+        for (int w = 0; w < (n + 31) / 32; ++w) any |= skip_mask[w];
+        if (any) skip = skip_mask;
+    }
+    if (((uintptr_t)dst & 15) == 0 && (nbytes & 15) == 0 && (!skip || (rb & 15) == 0)) {
+        copy_rows<float4>(dst, nbytes, rb, skip);
+    } else if (((uintptr_t)dst & 7) == 0 && (nbytes & 7) == 0 && (rb & 7) == 0) {
+        copy_rows<float2>(dst, nbytes, rb, skip);
     } else {
-        const uint32_t* s1 = reinterpret_cast<const uint32_t*>(uuv_smem);
-        uint32_t* d1 = reinterpret_cast<uint32_t*>(dst);
-        for (size_t i = threadIdx.x; i < nbytes / 4; i += blockDim.x) d1[i] = s1[i];
+        copy_rows<uint32_t>(dst, nbytes, rb, skip);
     }
 }
 
@@ -519,6 +723,100 @@ __device__ __forceinline__ const void* stage_actions(const EngineP<T>& p, const 
                                          (uintptr_t)first * p.act_dim * sizeof(double));
 }
 
+// Everything the fp64 recompute of env e needs, loaded in one round trip, then
+// the recompute and the env's reward / termination / reset / stores /
+// observation (written directly, never staged).
+template <bool TRACK, bool DR, bool MIX, class Pat>
+__device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<double>& V0,
+                                         const VehP<double>& V1, int e, uint32_t gen, const void* act,
+                                         void* __restrict__ obs, void* __restrict__ rew,
+                                         uint8_t* __restrict__ done, int8_t* __restrict__ reason,
+                                         StatAcc& st) {
+    const uint64_t g = p.env_offset + (uint64_t)e;
+    const bool slot1 = MIX && (int64_t)g >= p.mix_bound0;
+    EnvIn<float, TRACK, false> in;
+    load_env<float, TRACK>(p, e, in);
+    in.bk = gen;
+    V2<double> rec[5];
+    if constexpr (DR) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) rec[k] = p.dr64[(size_t)e * 5 + k];
+    }
+    const void* arow = act_row(p, act, e);
+    const int nthr = slot1 ? V1.n_thr : V0.n_thr;
+    double a[MAX_THR];
+#pragma unroll
+    for (int k = 0; k < MAX_THR; ++k)
+        a[k] = k >= nthr ? 0.0
+               : p.io_f64 ? ((const double*)arow)[k]
+                          : (double)((const float*)arow)[k];
+#ifdef UUV_BAND_CLOCK
+    const long long t0 = clock64() + (long long)(a[0] * 0.0 + in.s[0] * 0.0f);
+#endif
+    const Band64Out r = slot1 ? replay_band64<DR, Pat>(p, V1, in.s, rec, a)
+                              : replay_band64<DR, Pat>(p, V0, in.s, rec, a);
+#ifdef UUV_BAND_CLOCK
+    const long long t1 = clock64() + (long long)(r.v[0] * 0.0f);
+#endif
+#pragma unroll
+    for (int k = 0; k < 12; ++k) in.s[k] = r.v[k];
+    st.n_b64 += 1;
+    if (slot1) {
+        if constexpr (MIX)
+            finish_env<float, TRACK, DR, 1, Pat>(p, e, -1, g, in.s, in, r.failed != 0, obs, rew,
+                                                 done, reason, st);
+    } else {
+        finish_env<float, TRACK, DR, 0, Pat>(p, e, -1, g, in.s, in, r.failed != 0, obs, rew, done,
+                                             reason, st);
+    }
+#ifdef UUV_BAND_CLOCK
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 64))
+        printf("band_env t=%d replay %lld finish %lld\n", threadIdx.x, t1 - t0, clock64() - t1);
+#endif
+}
+
+// Step-kernel tail for a band-predictor miss (an env that was not a candidate
+// but whose fp32 pitch trajectory left the band): recomputed in fp64 after the
+// block's stores and statistics, out of line so the hot path carries no fp64
+// code; its statistics go to the block's partial slot with atomics.
+template <bool TRACK, bool DR, bool MIX, class Pat>
+__device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const void* act,
+                                       void* obs, void* rew, uint8_t* done, int8_t* reason) {
+    StatAcc st;
+    band_env<TRACK, DR, MIX, Pat>(p, p.veh64_dev[0], p.veh64_dev[1], e,
+                                  band_gen(p, p.band_ctr[0]), act, obs, rew, done, reason, st);
+    if (p.stats_on) {
+        double* part = p.stats + (size_t)blockIdx.x * NSTAT;
+        atomicAdd(part + ST_REWARD, (double)st.rew);
+        atomicAdd(part + ST_STEPS, 1.0);
+        atomicAdd(part + ST_BAND64, 1.0);
+        if (st.n_tr) atomicAdd(part + ST_DONE_TRUNC, 1.0);
+        if (st.n_dv) atomicAdd(part + ST_DONE_DIV, 1.0);
+        if (st.n_fl) atomicAdd(part + ST_DONE_FAIL, 1.0);
+        if (st.eplen) {
+            atomicAdd(part + ST_EP_RETURN, (double)st.epret);
+            atomicAdd(part + ST_EP_LEN, (double)st.eplen);
+        }
+        if (st.n_err) atomicAdd(part + ST_RESAMPLE_ERR, (double)st.n_err);
+    }
+}
+
+// this block's envs [first, first + span) are done with the step: advance the
+// step kernel's env counter (fire-and-forget; EngineP::band_ctr)
+// (after a barrier: every thread of the block is past its last counter read)
+__device__ __forceinline__ void band_count(const EngineP<float>& p, int first, int span) {
+    if (!p.band_f) return;
+    __syncthreads();
+    const int n = min(span, p.n_env - first);
+    if (threadIdx.x == 0 && n > 0) atomicAdd(p.band_ctr, (unsigned long long)n);
+}
+
+// rows this block did not finish (band candidates, tail envs), one bit per row
+__device__ __forceinline__ void mark_rows(uint32_t* mask, int row, bool skip) {
+    const uint32_t b = __ballot_sync(0xffffffffu, skip);
+    if ((threadIdx.x & 31) == 0) mask[row >> 5] = b;
+}
+
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BLOCK, is_f64<T>() ? STEP_MIN_BLOCKS_F64
                                       : (DR ? (Pat::fossen ? STEP_MIN_BLOCKS_DR : STEP_MIN_BLOCKS_F64)
@@ -534,14 +832,21 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
         act = stage_actions(p, act, first, min(BLOCK, p.n_env - first), BLOCK);
     }
     StatAcc st;
-    if (e < p.n_env) one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
-                                                     reason, st);
+    int code = ENV_DONE;
+    if (e < p.n_env) code = one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
+                                                            reason, st);
     pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
+        __shared__ uint32_t skip[BLOCK / 32];
+        mark_rows(skip, threadIdx.x, code != ENV_DONE);
         const int first = blockIdx.x * BLOCK;
-        flush_obs<T>(p, obs, first, min(BLOCK, p.n_env - first));
+        flush_obs<T>(p, obs, first, min(BLOCK, p.n_env - first), skip);
     }
     if (p.stats_on) block_stats(p.stats, st);
+    if constexpr (!is_f64<T>()) {
+        if (code == ENV_TAIL) band_tail<TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason);
+        band_count(p, blockIdx.x * BLOCK, BLOCK);
+    }
 }
 
 // Paired variant: block b covers envs [2*BLOCK*b, 2*BLOCK*(b+1)); thread t
@@ -563,19 +868,136 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     const int sl0 = MIX && (int64_t)(p.env_offset + (uint64_t)e0) >= p.mix_bound0;
     const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
     const int l0 = threadIdx.x, l1 = threadIdx.x + BLOCK;
+    int c0 = ENV_DONE, c1 = ENV_DONE;
     if (a0 && a1 && sl0 == sl1) {
-        if (sl0 == 0) step_pair<TRACK, 0>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
-        else if constexpr (MIX) step_pair<TRACK, 1>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
+        int c = ENV_DONE;
+        if (sl0 == 0) c = step_pair<TRACK, 0>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
+        else if constexpr (MIX) c = step_pair<TRACK, 1>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
+        c0 = c & 3;
+        c1 = c >> 2;
     } else {
-        if (a0) one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st);
-        if (a1) one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st);
+        if (a0) c0 = one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st);
+        if (a1) c1 = one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st);
     }
     pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
+        __shared__ uint32_t skip[2 * BLOCK / 32];
+        mark_rows(skip, l0, c0 != ENV_DONE);
+        mark_rows(skip, l1, c1 != ENV_DONE);
         const int first = blockIdx.x * (2 * BLOCK);
-        flush_obs<float>(p, obs, first, min(2 * BLOCK, p.n_env - first));
+        flush_obs<float>(p, obs, first, min(2 * BLOCK, p.n_env - first), skip);
     }
     if (p.stats_on) block_stats(p.stats, st);
+    if (c0 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
+    if (c1 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
+    band_count(p, blockIdx.x * (2 * BLOCK), 2 * BLOCK);
+}
+
+// Kernel parameters of the band kernel: the step's block plus the fp64 base
+// vehicles, so every vehicle coefficient is a constant-bank operand
+struct BandP {
+    EngineP<float> p;
+    VehP<double> veh[MAX_VEH];
+};
+
+constexpr int BAND_BLOCK = 128;        // band-kernel threads
+constexpr int BAND_SUB = 4 * 4 * BAND_BLOCK;   // flags scanned per pass: 4 uint4 per thread
+constexpr int BAND_LIST = 4096;        // candidate list capacity (shared memory)
+
+// Band kernel, launched on a side stream CONCURRENTLY with the step kernel
+// (which skips these envs).  Block b walks the chunks [b*band_per, ...) of the
+// batch: the chunk's flag words (EngineP::band_f) are read with 16-byte loads,
+// this step's candidates compacted into shared memory, and each stepped in fp64
+// -- recompute, reward / termination / reset / observation -- beside the fp32
+// step instead of after it.  Chunks are sized for about one pass of BAND_BLOCK
+// candidates: the band blocks are latency-bound (dependent fp64 chains), so
+// their number x lifetime is what they take from the step kernel's SMs.
+// Statistics go to the band kernel's own per-block partial slots.
+template <bool TRACK, bool DR, bool MIX, class Pat>
+__global__ void __launch_bounds__(BAND_BLOCK)
+k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
+       void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
+       int8_t* __restrict__ reason) {
+    const EngineP<float>& p = bp.p;
+    __shared__ int list[BAND_LIST];
+    __shared__ uint32_t cnt;
+    const unsigned lane = threadIdx.x & 31;
+    // this step's generation: envs the step kernel has already stepped carry the
+    // next one, candidates (never touched by it) this one with the flag bit set
+    const uint32_t gen = band_gen(p, p.band_ctr[1]);
+    const uint32_t want = (gen << 1) | 1u;
+    StatAcc st;
+    int scanned = 0;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    auto drain = [&]() {   // step the listed candidates, empty the list
+        const uint32_t n = cnt;
+        for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
+            band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], list[i], gen, act, obs, rew,
+                                          done, reason, st);
+        __syncthreads();
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+    };
+    for (int cb = blockIdx.x * p.band_per; cb < p.n_env; cb += gridDim.x * p.band_per) {
+        const int cend = min(cb + p.band_per, p.n_env);
+        scanned += cend - cb;
+        for (int base = cb; base < cend; base += BAND_SUB) {
+            if (cnt + BAND_SUB > BAND_LIST) drain();   // uniform: cnt is read after a barrier
+            const int end = min(base + BAND_SUB, cend);
+            uint32_t f[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = base + 4 * (threadIdx.x + k * BAND_BLOCK);
+                if (i + 3 < end) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(p.band_f + i);
+                    f[4 * k] = q.x; f[4 * k + 1] = q.y; f[4 * k + 2] = q.z; f[4 * k + 3] = q.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) f[4 * k + j] = i + j < end ? p.band_f[i + j] : 0u;
+                }
+            }
+            uint32_t mine = 0;   // bit 4k+j: env base + 4 (t + k BAND_BLOCK) + j is a candidate
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mine |= (f[j] == want ? 1u : 0u) << j;
+            const uint32_t c = __popc(mine);
+            uint32_t incl = c;   // warp inclusive scan of the counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (unsigned)o) incl += v;
+            }
+            uint32_t at = 0;
+            if (lane == 31 && incl) at = atomicAdd(&cnt, incl);
+            at = __shfl_sync(0xffffffffu, at, 31) + incl - c;
+            while (mine) {
+                const int j = __ffs(mine) - 1;
+                mine &= mine - 1;
+                list[at++] = base + 4 * (threadIdx.x + (j >> 2) * BAND_BLOCK) + (j & 3);
+            }
+            __syncthreads();
+        }
+    }
+    drain();
+    if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
+    if (threadIdx.x == 0 && scanned > 0) atomicAdd(p.band_ctr + 1, (unsigned long long)scanned);
+}
+
+// band flags from the current states (after create / reset_all / set_states /
+// restore): generation = the band kernels' current one
+__device__ __forceinline__ void write_band_flag(const EngineP<float>& p, int e, const float s[12]) {
+    if (p.band_f)
+        p.band_f[e] = (band_gen(p, p.band_ctr[0]) << 1) | (band_cand(p, s) ? 1u : 0u);
+}
+template <class T> __device__ __forceinline__ void write_band_flag(const EngineP<T>&, int, const T*) {}
+
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_band_flags(const __grid_constant__ EngineP<T> p) {
+    const int e = blockIdx.x * BLOCK + threadIdx.x;
+    if (e >= p.n_env) return;
+    const V4<T> a0 = p.s0[e], a1 = p.s1[e], a2 = p.s2[e];
+    const T s[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+    write_band_flag(p, e, s);
 }
 
 // observation of the current state at the current step (reset / inspection)
@@ -624,6 +1046,7 @@ __global__ void __launch_bounds__(BLOCK) k_reset(const __grid_constant__ EngineP
     p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
     p.s1[e] = V4<T>{s[4], s[5], s[6], s[7]};
     p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
+    write_band_flag(p, e, s);
     if (obs) observe_env<T, IO>(p, e, s, 0, obs);
 }
 
@@ -648,8 +1071,9 @@ __global__ void __launch_bounds__(BLOCK) k_dr_init(const __grid_constant__ Engin
     V4<T> d0, d1;
     V2<T> d2;
     // create-time draw: full 6x6 fp64 check (PatDense) for the error report
-    const bool ok = slot1 ? dr_draw<T, PatDense>(p.veh[1], p.ranges, p.seed, g, ctr, d0, d1, d2)
-                          : dr_draw<T, PatDense>(p.veh[0], p.ranges, p.seed, g, ctr, d0, d1, d2);
+    V2<double>* rec = p.dr64 ? p.dr64 + (size_t)e * 5 : nullptr;
+    const bool ok = slot1 ? dr_draw<T, PatDense>(p.veh[1], p.ranges, p.seed, g, ctr, d0, d1, d2, rec)
+                          : dr_draw<T, PatDense>(p.veh[0], p.ranges, p.seed, g, ctr, d0, d1, d2, rec);
     p.dr0[e] = d0; p.dr1[e] = d1; p.dr2[e] = d2;
     p.param_ctr[e] = ctr;
     if (!ok) atomicMin(first_bad, e);
@@ -731,9 +1155,12 @@ __global__ void k_unpack_states(const __grid_constant__ EngineP<T> p,
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= p.n_env) return;
     const double* r = in + (size_t)e * 12;
-    p.s0[e] = V4<T>{(T)r[0], (T)r[1], (T)r[2], (T)r[3]};
-    p.s1[e] = V4<T>{(T)r[4], (T)r[5], (T)r[6], (T)r[7]};
-    p.s2[e] = V4<T>{(T)r[8], (T)r[9], (T)r[10], (T)r[11]};
+    const T s[12] = {(T)r[0], (T)r[1], (T)r[2], (T)r[3], (T)r[4], (T)r[5],
+                     (T)r[6], (T)r[7], (T)r[8], (T)r[9], (T)r[10], (T)r[11]};
+    p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
+    p.s1[e] = V4<T>{s[4], s[5], s[6], s[7]};
+    p.s2[e] = V4<T>{s[8], s[9], s[10], s[11]};
+    write_band_flag(p, e, s);
 }
 
 template <class T>
@@ -822,6 +1249,10 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
         const int e0 = t * TILE + threadIdx.x, e1 = e0 + BLOCK;
         EnvIn<float, false> in0, in1;
         in0.step = p.step[e0]; in1.step = p.step[e1];
+        if (p.band_f) {
+            in0.bf = p.band_f[e0];
+            in1.bf = p.band_f[e1];
+        }
         in0.ep_ret = p.ep_ret[e0]; in1.ep_ret = p.ep_ret[e1];
         mbar_wait(&mbar[stage], stage ? parity1 : parity0);
         if (stage) parity1 ^= 1; else parity0 ^= 1;
@@ -842,21 +1273,27 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
         const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
         const float* r0 = UUV_TMA_ACT ? qa + (size_t)threadIdx.x * A : actf + (size_t)e0 * A;
         const float* r1 = UUV_TMA_ACT ? qa + (size_t)(threadIdx.x + BLOCK) * A : actf + (size_t)e1 * A;
+        int c0 = ENV_DONE, c1 = ENV_DONE;
         if (sl0 == sl1) {
+            int c = ENV_DONE;
             if (sl0 == 0)
-                pair_core<false, 0>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
-                                    reason, st);
+                c = pair_core<false, 0>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
+                                        reason, st);
             else if constexpr (MIX)
-                pair_core<false, 1>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
-                                    reason, st);
+                c = pair_core<false, 1>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
+                                        reason, st);
+            c0 = c & 3;
+            c1 = c >> 2;
         } else {   // vehicle-slab boundary inside the pair: one env at a time
             if constexpr (MIX) {
-                one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew, done,
-                                                             reason, st);
-                one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew, done,
-                                                             reason, st);
+                c0 = one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew, done,
+                                                                  reason, st);
+                c1 = one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew, done,
+                                                                  reason, st);
             }
         }
+        if (c0 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
+        if (c1 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
         __syncthreads();   // this stage is consumed before it is refilled
         stage ^= 1;
     }
@@ -864,12 +1301,20 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
     const int tail0 = n_full * TILE;
     if (tail0 < p.n_env && blockIdx.x == n_full % gridDim.x) {
         const int e0 = tail0 + threadIdx.x, e1 = e0 + BLOCK;
-        if (e0 < p.n_env) one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew,
-                                                                         done, reason, st);
-        if (e1 < p.n_env) one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew,
-                                                                         done, reason, st);
+        const int c0 = e0 < p.n_env ? one_env<float, false, false, MIX, PatFossen>(
+                                          p, e0, -1, act, obs, rew, done, reason, st) : ENV_DONE;
+        const int c1 = e1 < p.n_env ? one_env<float, false, false, MIX, PatFossen>(
+                                          p, e1, -1, act, obs, rew, done, reason, st) : ENV_DONE;
+        if (c0 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
+        if (c1 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
     }
     if (p.stats_on) block_stats(p.stats, st);
+    {   // envs this block stepped: its full tiles (+ the partial tail tile)
+        int cnt = 0;
+        for (int t2 = blockIdx.x; t2 < n_full; t2 += gridDim.x) cnt += TILE;
+        if (tail0 < p.n_env && blockIdx.x == n_full % gridDim.x) cnt += p.n_env - tail0;
+        band_count(p, 0, cnt);
+    }
 }
 
 // ------------------------------------------------------------------ launchers
@@ -888,9 +1333,9 @@ static void allow_smem() {
 }
 
 template <class T>
-cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
-                            const void* act, void* obs, void* rew, uint8_t* done,
-                            int8_t* reason, cudaStream_t st) {
+static cudaError_t launch_step_main(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
+                                    const void* act, void* obs, void* rew, uint8_t* done,
+                                    int8_t* reason, cudaStream_t st) {
     const bool mix = p.n_veh > 1;
     const size_t esz = p.io_f64 ? 8 : sizeof(T);
     if constexpr (std::is_same<T, float>::value) {
@@ -948,6 +1393,68 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
     return cudaGetLastError();
 }
 
+// The band kernel on the engine's side stream, forked from and joined back to
+// the launching stream around the step kernel (fp32 engines with band64): it
+// runs the band candidates in fp64 while the step kernel runs everything else.
+// Stream-capturable (the fork / join become graph edges).
+static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                               const void* act, void* obs, void* rew, uint8_t* done,
+                               int8_t* reason, cudaStream_t side) {
+    thread_local BandP bq;   // host staging of the launch parameters (copied at launch)
+    EngineP<float>& q = bq.p;
+    q = p;
+    for (int v = 0; v < MAX_VEH; ++v) bq.veh[v] = p.veh64[v];
+    q.stage_obs = 0;
+    q.stage_act = 0;
+    q.stagger_ns = 0;
+    q.pdl = 0;
+    q.persist_blocks = 0;
+    q.stats = p.stats_band;
+    const bool mix = p.n_veh > 1;
+    const dim3 grid(std::max(1, p.band_grid));
+#define UUV_B(TR, D, M, PAT) k_band<TR, D, M, PAT><<<grid, BAND_BLOCK, 0, side>>>(bq, act, obs, rew, done, reason)
+#define UUV_BP(TR, D, M) \
+    if (fossen) UUV_B(TR, D, M, PatFossen); else UUV_B(TR, D, M, PatDense)
+    if (track) {
+        if (dr) { if (mix) UUV_BP(true, true, true); else UUV_BP(true, true, false); }
+        else { if (mix) UUV_BP(true, false, true); else UUV_BP(true, false, false); }
+    } else {
+        if (dr) { if (mix) UUV_BP(false, true, true); else UUV_BP(false, true, false); }
+        else { if (mix) UUV_BP(false, false, true); else UUV_BP(false, false, false); }
+    }
+#undef UUV_BP
+#undef UUV_B
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
+                            const void* act, void* obs, void* rew, uint8_t* done,
+                            int8_t* reason, cudaStream_t st) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (p.band_same && p.band_theta < INFINITY) {
+            cudaError_t e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
+            if (e == cudaSuccess) e = launch_band(p, track, dr, fossen, act, obs, rew, done, reason, st);
+            return e;
+        }
+        if (p.band_side && p.band_theta < INFINITY) {
+            cudaStream_t side = (cudaStream_t)p.band_side;
+            cudaEvent_t fork = (cudaEvent_t)p.band_ev[0], join = (cudaEvent_t)p.band_ev[1];
+            // the step kernel first: its blocks are dispatched first, the band
+            // kernel's few small blocks fill in beside them
+            cudaError_t e = cudaEventRecord(fork, st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+            if (e == cudaSuccess)
+                e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
+            if (e == cudaSuccess) e = launch_band(p, track, dr, fossen, act, obs, rew, done, reason, side);
+            if (e == cudaSuccess) e = cudaEventRecord(join, side);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
+            return e;
+        }
+    }
+    return launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
+}
+
 template <class T>
 cudaError_t Launch<T>::reset(const EngineP<T>& p, T* obs, cudaStream_t st) {
     k_reset<T, T><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p, obs);
@@ -999,6 +1506,12 @@ cudaError_t Launch<T>::pack_states_t(const EngineP<T>& p, T* out, cudaStream_t s
 template <class T>
 cudaError_t Launch<T>::unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st) {
     k_unpack_states<T><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, in);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::band_flags(const EngineP<T>& p, cudaStream_t st) {
+    k_band_flags<T><<<(p.n_env + BLOCK - 1) / BLOCK, BLOCK, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -48,6 +48,8 @@ def _cfg0(kind, vehicle, n, seed, dr, episode_len, precision, lookahead, mixed, 
                                   env_offset=env_offset)
 
 
+WARM = 300   # free-running steps before the teacher-forced ones (tumbling envs present)
+
 CONFIGS = {
     "station_heavy": dict(),
     "station_bluerov2_dr": dict(vehicle="bluerov2", dr="create"),
@@ -70,6 +72,12 @@ CONFIGS = {
     "circle_3sub_fast": dict(kind="circle", vehicle="bluerov2", n_substeps=3,
                              control_dt=0.02, radius=2.5, angular_rate=0.6,
                              center=(1.0, -1.0), depth=1.5, episode_len=43),
+    # the exact kernels bench.py times (bench.py CONFIGS): C2 BlueROV2 station, no DR,
+    # 4,096 envs (k_step<float,0,0,0,Fossen>); C5 mixed station, no DR, paired kernel
+    # (k_step_pair<0,1>); C3 Heavy lemniscate + per-episode DR, 65,536 envs
+    "bench_c2": dict(vehicle="bluerov2", n=4096),
+    "bench_c5": dict(mixed=True, pair="on", n=131072),
+    "bench_c3": dict(kind="lemniscate", dr="episode", n=65536),
 }
 
 
@@ -113,16 +121,18 @@ def test_dr_factors(name):
 
 @pytest.mark.parametrize("name", list(CONFIGS))
 def test_single_step_teacher_forced(name):
-    """One control step from the oracle's own state, 36 times, every env.
+    """Strict single-step contract (BASELINE.json north_star).
 
-    Gate: terminations / reasons bit-exact (divergence ties excluded); reward
-    and state within 1e-6 + 1e-5|b| for envs outside the pitch band; beyond the
-    tolerance at most 1e-4 of the checked env-steps, none with |theta| <= 1 rad,
-    and never by 2x while |theta| <= 1.2 (measured: 2 of 145k env-steps at
-    1.1-1.3x, both at |theta| > 1.2 where sec/tan(theta) amplify the fp32
-    rounding of the input; with a 0.1 s control step one env at theta = 1.38
-    pitching at 4 rad/s flips phi by ~pi within the step and lands 14x out).
-    Observations: compared with the oracle's observe() at the GPU's state.
+    Both sides step from the SAME fp32-rounded state (s = f32(oracle state) is
+    set on the oracle AND the GPU), so the comparison isolates the kernel's
+    arithmetic from input rounding.  The oracle first free-runs with the GPU for
+    ``WARM`` steps under bench actions, so the batch holds tumbling envs (the
+    pitch band is populated), not only fresh resets.  Gate, with ZERO exceptions:
+    every env with |theta_in| <= 1.4 rad has reward and all 12 state components
+    within 1e-6 + 1e-5|b| (angles mod 2 pi) -- including envs that pitch into the
+    band during the step (the engine steps those in fp64, see DESIGN.md §4);
+    terminations and reasons bit-exact (divergence-radius ties excluded and
+    counted); observations = the oracle's observe() at the GPU state.
     """
     cfg = _cfg(**CONFIGS[name])
     gpu = uuv.B200EnvBatch(cfg)
@@ -130,35 +140,39 @@ def test_single_step_teacher_forced(name):
     at_gpu = orc.OracleBatch(cfg)          # evaluates observe() at the GPU state
     act = orc.bench_actions(cfg["seed"], ref.num_envs, ref.action_dim)
     cols = P.obs_angle_cols(gpu.obs_dim)
-    n_checked = n_band = n_out = 0
+    for _ in range(WARM):
+        gpu.step_ex(act)
+        ref.step(act)
+    rc_g, pc_g = gpu.counters()
+    rc_r, pc_r = ref.counters()
+    synced = (rc_g == rc_r) & (pc_g == pc_r)   # a divergence tie desyncs an env's RNG
+    assert synced.mean() > 0.99
+    n_checked = n_band = 0
     worst = 0.0
-    n_steps = 36
+    n_steps = 24
     for t in range(n_steps):
-        s_in = ref.states()
-        gpu.set_states(s_in)
+        s = P.f32(ref.states())
+        ref.set_states(s)
+        gpu.set_states(s)
         gpu.set_step_counts(ref.step_counts())
         og, rg, dg, qg = gpu.step_ex(act)
         orr, rr, dr, qr = ref.step(act, with_reason=True)
         sr = ref.states()
-        band = (np.abs(s_in[:, 4]) > P.PITCH_BAND) | (np.abs(sr[:, 4]) > P.PITCH_BAND)
-        n_band += int(band.sum())
+        gate = (np.abs(s[:, 4]) <= P.PITCH_BAND) & synced
+        n_band += int((~gate).sum())
         tie = np.abs(-rr - 10.0) < 1e-4
-        assert np.array_equal(dg[~tie], dr[~tie]), f"done mismatch at t={t}"
-        assert np.array_equal(qg[~tie], qr[~tie]), f"reason mismatch at t={t}"
-        ok = ~band & ~tie
+        ok = gate & ~tie
+        assert np.array_equal(dg[ok], dr[ok]), f"done mismatch at t={t}"
+        assert np.array_equal(qg[ok], qr[ok]), f"reason mismatch at t={t}"
         assert P.within_tol(rg[ok], rr[ok]).all(), "reward outside tolerance"
         sg = gpu.states()
         live = ok & ~dr
         err = P.abs_err(sg[live], sr[live], P.STATE_ANGLES)
         scaled = err / (P.ABS_TOL + P.REL_TOL * np.abs(sr[live]))
-        out = (scaled > 1.0).any(axis=1)
-        n_out += int(out.sum())
-        th = np.maximum(np.abs(s_in[live, 4]), np.abs(sr[live, 4]))
-        conditioned = th <= 1.2
-        if conditioned.any():
-            worst = max(worst, float(scaled[conditioned].max()))
-        calm = th <= 1.0
-        assert not (out & calm).any(), "state outside tolerance at |theta| <= 1"
+        if scaled.size:
+            worst = max(worst, float(scaled.max()))
+        bad = np.flatnonzero(live)[(scaled > 1.0).any(axis=1)]
+        assert bad.size == 0, (t, bad[:5].tolist(), s[bad[:5], 4].tolist(), float(scaled.max()))
         # finished envs restart from an exactly-rounded reset draw
         fin = ok & dr
         assert np.array_equal(sg[fin], P.f32(sr[fin]))
@@ -166,11 +180,10 @@ def test_single_step_teacher_forced(name):
         at_gpu.set_states(sg)
         at_gpu.set_step_counts(gpu.step_counts())
         want_obs = at_gpu.observe()
-        assert P.within_tol(og, want_obs, cols).all(), "obs outside tolerance"
+        assert P.within_tol(og[gate], want_obs[gate], cols).all(), "obs outside tolerance"
         n_checked += int(live.sum())
-    assert worst < 2.0, worst
-    assert n_out <= 1e-4 * n_checked, (n_out, n_checked)
-    assert n_checked > 0.95 * n_steps * gpu.num_envs - n_band
+    assert worst <= 1.0, worst
+    assert n_checked > 0.9 * n_steps * gpu.num_envs - n_band
 
 
 @pytest.mark.parametrize("name", ["station_heavy", "lemniscate_heavy_drep", "mixed_station_dr",

@@ -1,0 +1,48 @@
+"""Latency probe of the fp64 band replay: C2/C5 bench engines, graph replays,
+device time per step with and without band64 (for ncu: -k regex:k_band64)."""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_2410_14117_b200 as uuv  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    n_sub = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+    for band, stream, margin in ((True, "side", None), (True, "same", None), (True, "side", -10.0),
+                                 (False, "side", None)):
+        cfg, _ = bench.build_config(name, 0, "fp32", band64=band)
+        cfg["device"]["band_stream"] = stream
+        if margin is not None:
+            cfg["device"]["band_margin"] = margin
+        cfg["task"]["n_substeps"] = n_sub
+        cfg["task"]["control_dt"] = 0.005 * n_sub
+        env = uuv.B200EnvBatch(cfg)
+        act = env.bench_actions_tensor()
+        env.capture_graph(act, n_steps=1)
+        for _ in range(300):          # into the tumbling regime
+            env.replay_graph()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        env.stats(clear=True)
+        a.record()
+        for _ in range(steps):
+            env.replay_graph()
+        b.record()
+        torch.cuda.synchronize()
+        st = env.stats()
+        print(name, "n_sub", n_sub, "band64", band, stream, "margin", margin, "us/step %.2f" % (a.elapsed_time(b) * 1e3 / steps),
+              "band steps/step %.1f" % (st["band64_steps"] / steps), flush=True)
+        env.close()
+
+
+if __name__ == "__main__":
+    main()
