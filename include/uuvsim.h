@@ -89,6 +89,11 @@ int32_t uuvsim_counters(uint64_t handle, uint64_t* reset_ctr, uint64_t* param_ct
 /* per-env randomised parameter record [M][10]:
  * f_mass f_added f_dlin f_dquad f_thrust rb_x rb_y rb_z weight buoyancy */
 int32_t uuvsim_dr_factors(uint64_t handle, double* out, uint64_t len);
+/* body wrench tau [M][6] of every env for f64 action rows [M][A] (the step's
+ * thruster map, thrusters.py:97-119, incl. the randomised thrust factor);
+ * inspection / force-output parity */
+int32_t uuvsim_wrench(uint64_t handle, const double* actions, uint64_t actions_len, double* out,
+                      uint64_t out_len);
 /* episode statistics [9]: sum reward, dones by reason (trunc, div, fail),
  * sum of completed-episode returns, sum of their lengths, env-steps,
  * rejected per-episode resamples, fp32 env-steps recomputed in fp64 because

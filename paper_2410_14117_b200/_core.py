@@ -49,6 +49,7 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
         "uuvsim_set_step_counts": (i32, [u64, vp, u64]),
         "uuvsim_counters": (i32, [u64, vp, vp, u64]),
         "uuvsim_dr_factors": (i32, [u64, vp, u64]),
+        "uuvsim_wrench": (i32, [u64, vp, u64, vp, u64]),
         "uuvsim_stats": (i32, [u64, vp, u64, i32]),
         "uuvsim_info": (i64, [u64, cp, u64]),
         "uuvsim_dev_step": (i32, [u64, vp, u64, vp, u64, vp, u64, vp, u64, vp, u64, u64]),

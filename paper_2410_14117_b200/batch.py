@@ -229,6 +229,17 @@ class B200EnvBatch:
         _core.check(self._lib, self._lib.uuvsim_dr_factors(self._handle, _ptr(out), out.size))
         return out
 
+    def wrench(self, actions) -> np.ndarray:
+        """Body wrench tau [N, 6] of every env for the given actions (the step
+        kernel's thruster map, reference thrusters.py:97-119)."""
+        act = np.ascontiguousarray(actions, dtype=np.float64)
+        if act.shape != (self.num_envs, self.action_dim):
+            raise ValueError(f"actions must have shape {(self.num_envs, self.action_dim)}")
+        out = np.zeros((self.num_envs, 6))
+        _core.check(self._lib, self._lib.uuvsim_wrench(self._handle, _ptr(act), act.size,
+                                                       _ptr(out), out.size))
+        return out
+
     def stats(self, clear: bool = False) -> dict:
         out = np.zeros(len(STAT_NAMES))
         _core.check(self._lib, self._lib.uuvsim_stats(self._handle, _ptr(out), len(STAT_NAMES), int(clear)))

@@ -226,6 +226,17 @@ int32_t uuvsim_dr_factors(uint64_t h, double* out, uint64_t len) {
     });
 }
 
+int32_t uuvsim_wrench(uint64_t h, const double* actions, uint64_t actions_len, double* out,
+                      uint64_t out_len) {
+    return with_engine(h, [&](uuv::Engine& e) {
+        const uint64_t na = (uint64_t)e.num_envs() * e.action_dim(), nt = (uint64_t)e.num_envs() * 6;
+        if (!actions || actions_len != na) return bad_size("action", na, "f64");
+        if (!out || out_len != nt) return bad_size("wrench", nt, "f64");
+        e.wrench_host(actions, out);
+        return UUVSIM_OK;
+    });
+}
+
 int32_t uuvsim_stats(uint64_t h, double* out, uint64_t len, int32_t clear) {
     return with_engine(h, [&](uuv::Engine& e) {
         if (!out || len != (uint64_t)uuv::NSTAT) return bad_size("stats", uuv::NSTAT, "f64");

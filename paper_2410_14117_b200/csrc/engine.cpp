@@ -1049,6 +1049,20 @@ void Engine::counters_host(uint64_t* rc, uint64_t* pc) {
     cuda_check(cudaStreamSynchronize(stream_), "ctr sync");
 }
 
+// body wrench tau [N][6] for host f64 action rows (thrusters.py:97-119): the
+// step kernel's wrench() in the engine precision
+void Engine::wrench_host(const double* act, double* out) {
+    activate();
+    ensure_staging();
+    ensure_pack();
+    const size_t N = (size_t)m_;
+    cuda_check(cudaMemcpyAsync(d_act64_, act, N * n_act_ * 8, cudaMemcpyHostToDevice, stream_), "act H2D");
+    if (fp64_) cuda_check(Launch<double>::wrench(*pd_, ranges_.enabled, d_act64_, d_pack_, stream_), "wrench");
+    else cuda_check(Launch<float>::wrench(*pf_, ranges_.enabled, d_act64_, d_pack_, stream_), "wrench");
+    cuda_check(cudaMemcpyAsync(out, d_pack_, N * 6 * 8, cudaMemcpyDeviceToHost, stream_), "wrench D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "wrench sync");
+}
+
 void Engine::dr_factors_host(double* out) {
     activate();
     if (!ranges_.enabled) {

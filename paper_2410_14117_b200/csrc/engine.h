@@ -79,6 +79,7 @@ public:
     void set_step_counts_host(const int64_t* in);
     void counters_host(uint64_t* reset_ctr, uint64_t* param_ctr);
     void dr_factors_host(double* out);     // [M][10]
+    void wrench_host(const double* act, double* out);   // [M][A] -> [M][6]
     void stats_host(double* out, bool clear);
 
     // exact slab checkpoint: header + the per-env device state (states, step

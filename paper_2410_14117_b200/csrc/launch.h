@@ -84,6 +84,8 @@ template <class T> struct Launch {
     static cudaError_t unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st);
     static cudaError_t pack_dr(const EngineP<T>& p, double* out, cudaStream_t st);
     static cudaError_t band_flags(const EngineP<T>& p, cudaStream_t st);
+    static cudaError_t wrench(const EngineP<T>& p, bool dr, const double* act, double* out,
+                              cudaStream_t st);
     static cudaError_t step_attrs(cudaFuncAttributes* a, bool track, bool dr, bool fossen,
                                   bool mix, bool pair, bool tma);
     static cudaError_t to_f64(const T* in, double* out, size_t n, cudaStream_t st);

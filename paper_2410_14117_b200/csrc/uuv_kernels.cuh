@@ -1163,6 +1163,25 @@ __global__ void k_unpack_states(const __grid_constant__ EngineP<T> p,
     write_band_flag(p, e, s);
 }
 
+// Body wrench of every env for f64 action rows [N][A] (thrusters.py:97-119,
+// inspection / parity): the step kernel's own wrench() with the env's
+// randomised thrust factor -> out [N][6] f64
+template <class T, bool DR>
+__global__ void k_wrench(const __grid_constant__ EngineP<T> p, const double* __restrict__ act,
+                         double* __restrict__ out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= p.n_env) return;
+    const bool slot1 = p.n_veh > 1 && (int64_t)(p.env_offset + (uint64_t)e) >= p.mix_bound0;
+    EnvParams<T, DR> E;
+    if constexpr (DR) E.f_thrust = p.dr1[e].x;
+    T tau[6];
+    const double* row = act + (size_t)e * p.act_dim;
+    if (slot1) wrench<T, DR, DR>(p.veh[1], E, row, true, tau);
+    else wrench<T, DR, DR>(p.veh[0], E, row, true, tau);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) out[(size_t)e * 6 + i] = (double)tau[i];
+}
+
 template <class T>
 __global__ void k_pack_dr(const __grid_constant__ EngineP<T> p, double* __restrict__ out) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1506,6 +1525,14 @@ cudaError_t Launch<T>::pack_states_t(const EngineP<T>& p, T* out, cudaStream_t s
 template <class T>
 cudaError_t Launch<T>::unpack_states(const EngineP<T>& p, const double* in, cudaStream_t st) {
     k_unpack_states<T><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, in);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t Launch<T>::wrench(const EngineP<T>& p, bool dr, const double* act, double* out,
+                              cudaStream_t st) {
+    if (dr) k_wrench<T, true><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, act, out);
+    else k_wrench<T, false><<<(p.n_env + 255) / 256, 256, 0, st>>>(p, act, out);
     return cudaGetLastError();
 }
 

@@ -13,6 +13,8 @@ import paper_2410_14117_b200 as uuv
 from oracle import oracle as orc
 from tests import parity as P
 
+MAX_THR = 8
+
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
@@ -509,3 +511,49 @@ def test_tma_pipelined_kernel_bit_identical():
     sa, sb = a.stats(), b.stats()
     assert sa["env_steps"] == sb["env_steps"] == 25 * n
     assert sa["done_truncation"] == sb["done_truncation"] > 0
+
+
+@pytest.mark.parametrize("name", ["station_heavy", "station_bluerov2_dr", "mixed_station_dr",
+                                  "bench_c3"])
+def test_wrench_matches_oracle(name):
+    """Force output: the body wrench tau the step applies (thruster curve x
+    randomised thrust factor x allocation, reference thrusters.py:97-119) against
+    the oracle's _wrench_flat for the env's own parameters, for clamped, in-range
+    and zero throttles.  tau_r = sum_i A_ri F_i is a sum of thrust contributions
+    of up to ~50 N that cancel (symmetric layouts), so the fp32 tolerance
+    rel 1e-5 / abs 1e-6 is applied to the magnitude of that sum's terms,
+    |d tau_r| <= 1e-6 + 1e-5 sum_i |A_ri F_i| -- the scale fp32 can resolve;
+    against |tau_r| alone an exact cancellation (tau_r = 0 in fp64) leaves fp32
+    rounding of the terms (~1e-6 N) that no fp32 evaluation avoids."""
+    import ctypes
+    cfg = _cfg(**CONFIGS[name])
+    gpu = uuv.B200EnvBatch(cfg)
+    ref = orc.OracleBatch(cfg)
+    n, a = gpu.num_envs, gpu.action_dim
+    act = 1.3 * orc.bench_actions(cfg["seed"] + 5, n, a)     # some beyond the clamp
+    act[::7] = 0.0
+    tau = gpu.wrench(act)
+    L = orc.lib()
+    envs = np.unique(np.linspace(0, n - 1, 512).astype(int))
+    want = np.zeros((envs.size, 6))
+    scale = np.zeros((envs.size, 6))
+    for i, e in enumerate(envs):
+        kp = ref.kparams(int(e))
+        row = np.ascontiguousarray(act[e])
+        out = np.zeros(6)
+        L.orc_wrench(ctypes.byref(kp), row.ctypes.data_as(ctypes.c_void_p),
+                     out.ctypes.data_as(ctypes.c_void_p))
+        want[i] = out
+        nt = kp.n_thr
+        t = np.clip(row[:nt], -1.0, 1.0)
+        curve = np.array(kp.curve)[:nt]
+        f = np.array(kp.kmax)[:nt] * np.where(curve == 0, t, t * np.abs(t))
+        scale[i] = np.abs(np.array(kp.alloc).reshape(6, MAX_THR)[:, :nt] * f).sum(axis=1)
+    err = np.abs(tau[envs] - want)
+    bad = err > P.ABS_TOL + P.REL_TOL * scale
+    assert not bad.any(), (np.argwhere(bad)[:5].tolist(), err[bad][:5].tolist())
+    # the unscaled rel/abs form holds wherever the sum does not cancel
+    big = np.abs(want) > 0.1 * scale
+    assert P.within_tol(tau[envs][big], want[big]).all()
+    gpu.close()
+    ref.close()
