@@ -13,8 +13,6 @@ import paper_2410_14117_b200 as uuv
 from oracle import oracle as orc
 from tests import parity as P
 
-MAX_THR = 8
-
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
@@ -548,7 +546,7 @@ def test_wrench_matches_oracle(name):
         t = np.clip(row[:nt], -1.0, 1.0)
         curve = np.array(kp.curve)[:nt]
         f = np.array(kp.kmax)[:nt] * np.where(curve == 0, t, t * np.abs(t))
-        scale[i] = np.abs(np.array(kp.alloc).reshape(6, MAX_THR)[:, :nt] * f).sum(axis=1)
+        scale[i] = np.abs(np.array(kp.alloc)[:6 * nt].reshape(6, nt) * f).sum(axis=1)   # [6][n_thr]
     err = np.abs(tau[envs] - want)
     bad = err > P.ABS_TOL + P.REL_TOL * scale
     assert not bad.any(), (np.argwhere(bad)[:5].tolist(), err[bad][:5].tolist())
