@@ -103,7 +103,11 @@ int32_t uuvsim_stats(uint64_t handle, double* out, uint64_t len, int32_t clear);
 /* JSON description of the engine (precision, grid, registers, device) */
 int64_t uuvsim_info(uint64_t handle, char* buf, uint64_t cap);
 
-/* device face: all pointers are device memory; stream = cudaStream_t (0 = legacy).
+/* Ordering: host-ABI calls (uuvsim_step, _states, ...) run on the engine's own
+ * stream and wait for the engine's last device-face launch (recorded outside
+ * stream capture), so device-face then host-ABI calls need no explicit sync.
+ *
+ * device face: all pointers are device memory; stream = cudaStream_t (0 = legacy).
  * actions/obs/rew elements are the engine precision: float for "fp32" engines
  * (default), double for "fp64" engines (see uuvsim_info). */
 int32_t uuvsim_dev_step(uint64_t handle, const void* actions, uint64_t actions_len, void* obs,
@@ -157,7 +161,10 @@ int32_t uuvsim_dev_pd_actions(uint64_t handle, const UuvPdGains* gains, const vo
 int32_t uuvsim_dev_states(uint64_t handle, void* out, uint64_t len, uint64_t stream);
 int32_t uuvsim_dev_stats(uint64_t handle, double* out, uint64_t len, int32_t clear,
                          uint64_t stream);
-/* capture n_steps consecutive device steps on fixed buffers into a CUDA graph */
+/* capture n_steps consecutive device steps on fixed buffers into a CUDA graph.
+ * Buffers as for uuvsim_dev_step: actions [M][A], obs [M][obs_dim] (16-byte
+ * aligned), rew [M], done [M], reason [M] or NULL, elements in the engine
+ * precision; they must stay valid while the graph is replayed. */
 int32_t uuvsim_dev_graph_capture(uint64_t handle, const void* actions, void* obs, void* rew,
                                  uint8_t* done, int8_t* reason, uint32_t n_steps);
 int32_t uuvsim_dev_graph_launch(uint64_t handle, uint64_t stream);

@@ -6,6 +6,7 @@ sub-stepped Fossen 6-DOF dynamics, reward/termination, counter-RNG auto-reset
 and domain randomisation, fused into one sm_100a CUDA kernel per step.
 """
 
+from ._core import NativeError
 from .batch import (STAT_NAMES, B200EnvBatch, batch_create, bench_actions, bench_throughput,
                     resolve_backend)
 from .config import (CIRCLE, HELIX, LEMNISCATE, STATION_KEEPING, ConfigError, ParamsError,
@@ -16,7 +17,7 @@ from .config import (CIRCLE, HELIX, LEMNISCATE, STATION_KEEPING, ConfigError, Pa
 __version__ = "0.1.0"
 
 __all__ = [
-    "B200EnvBatch", "CIRCLE", "ConfigError", "HELIX", "LEMNISCATE", "ParamsError",
+    "B200EnvBatch", "CIRCLE", "ConfigError", "HELIX", "LEMNISCATE", "NativeError", "ParamsError",
     "RandomizationRanges", "STATION_KEEPING", "STAT_NAMES", "TaskSpec", "VehicleParams",
     "batch_create", "bench_actions", "bench_throughput", "bluerov2_params", "default_params",
     "default_ranges", "engine_config_dict", "engine_config_json", "load_params",

@@ -53,6 +53,7 @@ class B200EnvBatch:
         _core.check(lib, lib.uuvsim_create(text.encode("utf-8"), ctypes.byref(handle)))
         self._handle = handle.value
         self._open = True
+        self._registered = {}   # device buffers the engine writes into (kept alive here)
         spec = (ctypes.c_uint64 * 4)()
         _core.check(lib, lib.uuvsim_spec(self._handle, spec))
         self.num_envs, self.obs_dim, self.action_dim, self.episode_len = (int(x) for x in spec)
@@ -148,6 +149,7 @@ class B200EnvBatch:
         if getattr(self, "_open", False):
             self._lib.uuvsim_destroy(self._handle)
             self._open = False
+            self._registered = {}
 
     def _require_open(self):
         if not self._open:
@@ -329,16 +331,36 @@ class B200EnvBatch:
     def set_done_f32(self, buf) -> None:
         """Register (tensor) or clear (None) a float32 [num_envs] device buffer
         later device-face steps also write done into as 0.0 / 1.0
-        (uuvsim_dev_set_done_f32)."""
+        (uuvsim_dev_set_done_f32).  The batch keeps a reference to the tensor
+        while it is registered: the engine writes into its memory."""
         self._require_open()
         if buf is None:
             _core.check(self._lib, self._lib.uuvsim_dev_set_done_f32(self._handle, None, 0))
+            self._registered.pop("done_f32", None)
             return
         import torch
         if buf.dtype != torch.float32 or not buf.is_cuda or not buf.is_contiguous():
             raise ValueError("done buffer must be a contiguous float32 CUDA tensor")
         _core.check(self._lib, self._lib.uuvsim_dev_set_done_f32(
             self._handle, buf.data_ptr(), buf.numel()))
+        self._registered["done_f32"] = buf
+
+    def set_final_obs(self, buf) -> None:
+        """Register (tensor) or clear (None) a [num_envs, obs_dim] device buffer the
+        step writes finished envs' TERMINAL observations into
+        (uuvsim_dev_set_final_obs); referenced by the batch while registered."""
+        self._require_open()
+        if buf is None:
+            _core.check(self._lib, self._lib.uuvsim_dev_set_final_obs(self._handle, None, 0))
+            self._registered.pop("final_obs", None)
+            return
+        if (buf.dtype != self.dtype or not buf.is_cuda or not buf.is_contiguous() or
+                buf.numel() != self.num_envs * self.obs_dim):
+            raise ValueError(f"final_obs must be a contiguous {self.dtype} CUDA tensor of "
+                             f"{self.num_envs * self.obs_dim} elements")
+        _core.check(self._lib, self._lib.uuvsim_dev_set_final_obs(
+            self._handle, buf.data_ptr(), buf.numel()))
+        self._registered["final_obs"] = buf
 
     def set_pdl(self, on: bool = True) -> None:
         """Launch later device-face steps as programmatic dependents of the previous

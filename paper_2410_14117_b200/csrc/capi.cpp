@@ -395,6 +395,12 @@ int32_t uuvsim_dev_graph_capture(uint64_t h, const void* act, void* obs, void* r
     return with_engine(h, [&](uuv::Engine& e) {
         if (!act || !obs || !rew || !done) return fail(UUVSIM_ERR_SIZE, "null buffer");
         if (n_steps < 1) return fail(UUVSIM_ERR_SIZE, "n_steps must be >= 1");
+        // the same alignment contract as uuvsim_dev_step (vector row stores / loads);
+        // sizes are those of uuvsim_dev_step (documented in uuvsim.h)
+        const size_t esz = e.is_fp64() ? 8 : 4;
+        if (int32_t c = misaligned("obs", obs, 16)) return c;
+        if (int32_t c = misaligned("actions", act, esz)) return c;
+        if (int32_t c = misaligned("rew", rew, esz)) return c;
         e.graph_capture(act, obs, rew, done, reason, (int)n_steps);
         return UUVSIM_OK;
     });

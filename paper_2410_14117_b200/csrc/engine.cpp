@@ -309,6 +309,14 @@ void Engine::parse(const std::string& text) {
     }
     if (veh_.size() > 1 && mix_.empty())
         throw ConfigError("several vehicles need batch.vehicle_mix");
+    if (!mix_.empty()) {   // the global mix must cover this slab's envs
+        int64_t total = 0;
+        for (int64_t c : mix_) total += c;
+        if (total < (int64_t)env_offset_ + m_)
+            throw ConfigError("batch.vehicle_mix covers " + std::to_string(total) +
+                              " envs, fewer than env_offset + num_envs = " +
+                              std::to_string((int64_t)env_offset_ + m_));
+    }
     // device section (extension; unknown keys are ignored like serde)
     if (const json* d = opt(doc, "device")) {
         if (const json* v = opt(*d, "precision")) {
@@ -352,6 +360,10 @@ void Engine::parse(const std::string& text) {
             band64_ = v->get<bool>();
         }
         if (const json* v = opt(*d, "band_margin")) band_margin_ = num(*v, "device.band_margin");
+        if (const json* v = opt(*d, "band_tail")) {   // A/B: misses stay fp32
+            if (!v->is_boolean()) throw ConfigError("device.band_tail must be a bool");
+            band_tail_ = v->get<bool>();
+        }
         if (const json* v = opt(*d, "band_stream")) {   // "side" (concurrent) | "same" (A/B)
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "side") band_same_ = false;
@@ -495,7 +507,9 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.veh64 = veh64_.empty() ? nullptr : veh64_.data();
     p.sub_dt64 = task_.control_dt / (double)task_.n_substeps;
     p.veh64_dev = d_veh64_;
+    p.err_flag = d_err_;
     p.band_theta = band_grid_ > 0 ? BAND_THETA : INFINITY;
+    p.band_exit_theta = band_tail_ ? p.band_theta : INFINITY;
     p.band_kdt = (float)task_.control_dt;
     p.band_margin = (float)(band_margin_ >= -1e30 ? band_margin_
                                                    : 0.01 + 8.0 * task_.control_dt * task_.control_dt);
@@ -590,12 +604,12 @@ void Engine::allocate() {
     nblk_ = (int)((m_ + BLOCK - 1) / BLOCK);
     // per-block statistics partials: the step kernel's blocks, then the band
     // replay kernel's (fp32 engines with band64)
-    // band kernel: chunks of n/64 envs (2,048-16,384, a multiple of 2,048): about
-    // one pass of candidates per block, few long-lived blocks beside the step
+    // band kernel: chunks of n/256 envs (2,048-8,192, a multiple of 2,048): a
+    // few dozen candidates per block (one pass), spread over the SMs
     if (!fp64_ && band64_) {
-        const int64_t per = std::min<int64_t>(16384, std::max<int64_t>(2048, (m_ / 64 + 2047) / 2048 * 2048));
+        const int64_t per = std::min<int64_t>(8192, std::max<int64_t>(2048, (m_ / 256 + 2047) / 2048 * 2048));
         band_per_ = (int)per;
-        band_grid_ = (int)std::min<int64_t>(65536, (m_ + per - 1) / per);
+        band_grid_ = (int)((m_ + per - 1) / per);
     }
     // per-block statistics partials: the step kernel's blocks, then the band kernel's
     nstat_blk_ = nblk_ + band_grid_;
@@ -628,6 +642,11 @@ void Engine::allocate() {
         }
     }
     cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "cudaMalloc(flag)");
+    if (ranges_.enabled && ranges_.per_episode) {   // rejected-resample flag, mapped page-locked
+        cuda_check(cudaHostAlloc((void**)&h_err_, sizeof(int32_t), cudaHostAllocMapped), "cudaHostAlloc(err)");
+        *h_err_ = 0;
+        cuda_check(cudaHostGetDevicePointer((void**)&d_err_, (void*)h_err_, 0), "err flag alias");
+    }
     {   // fp32 register pack per vehicle (uuv_model.cuh RegPack layout)
         std::vector<float> pk((size_t)MAX_VEH * PACK_F4 * 4, 0.0f);
         for (size_t vi = 0; vi < veh_.size(); ++vi) {
@@ -657,6 +676,7 @@ void Engine::allocate() {
                    "vpack");
     }
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&dev_ev_, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 // host-ABI staging (f64 action / obs / reward rows, fp32 twins, done / reason
@@ -763,6 +783,9 @@ void Engine::release() {
         if (b) cudaFree(b);
     d_veh64_ = nullptr;
     d_band_f_ = nullptr;
+    if (h_err_) cudaFreeHost((void*)h_err_);
+    h_err_ = nullptr;
+    d_err_ = nullptr;
     if (band_side_) cudaStreamDestroy(band_side_);
     band_side_ = nullptr;
     for (auto& ev : band_ev_) {
@@ -775,6 +798,8 @@ void Engine::release() {
     d_vpack_ = nullptr;
     if (stream_) cudaStreamDestroy(stream_);
     stream_ = nullptr;
+    if (dev_ev_) cudaEventDestroy(dev_ev_);
+    dev_ev_ = nullptr;
 }
 
 void Engine::init_randomization() {   // engine.rs:440-458: per-env sample at create
@@ -809,6 +834,7 @@ template <class T> void Engine::reset_host_T(uint64_t seed, double* obs) {
 
 void Engine::reset_host(uint64_t seed, double* obs) {
     activate();
+    wait_device_face();
     if (fp64_) reset_host_T<double>(seed, obs);
     else reset_host_T<float>(seed, obs);
 }
@@ -996,12 +1022,19 @@ void Engine::step_host_T(const double* act, double* obs, double* rew, uint8_t* d
 void Engine::step_host(const double* act, double* obs, double* rew, uint8_t* done,
                        int8_t* reason) {
     activate();
+    wait_device_face();
+    if (h_err_) *h_err_ = 0;
     if (fp64_) step_host_T<double>(act, obs, rew, done, reason);
     else step_host_T<float>(act, obs, rew, done, reason);
+    if (h_err_ && *h_err_)   // engine.rs:553-558 panics here; the outputs are still written
+        throw RuntimeError("per-episode parameter resample rejected: randomized parameters "
+                           "invalid: M_RB + M_A is not positive definite (the env keeps its "
+                           "previous parameters)");
 }
 
 void Engine::states_host(double* out) {
     activate();
+    wait_device_face();
     ensure_pack();
     if (fp64_) cuda_check(Launch<double>::pack_states(*pd_, d_pack_, stream_), "pack");
     else cuda_check(Launch<float>::pack_states(*pf_, d_pack_, stream_), "pack");
@@ -1011,6 +1044,7 @@ void Engine::states_host(double* out) {
 
 void Engine::set_states_host(const double* in) {
     activate();
+    wait_device_face();
     ensure_pack();
     cuda_check(cudaMemcpyAsync(d_pack_, in, (size_t)m_ * 12 * 8, cudaMemcpyHostToDevice, stream_), "states H2D");
     if (fp64_) cuda_check(Launch<double>::unpack_states(*pd_, d_pack_, stream_), "unpack");
@@ -1020,6 +1054,7 @@ void Engine::set_states_host(const double* in) {
 
 void Engine::step_counts_host(int64_t* out) {
     activate();
+    wait_device_face();
     std::vector<int32_t> tmp((size_t)m_);
     int32_t* src = fp64_ ? pd_->step : pf_->step;
     cuda_check(cudaMemcpyAsync(tmp.data(), src, (size_t)m_ * 4, cudaMemcpyDeviceToHost, stream_), "steps D2H");
@@ -1029,6 +1064,7 @@ void Engine::step_counts_host(int64_t* out) {
 
 void Engine::set_step_counts_host(const int64_t* in) {
     activate();
+    wait_device_face();
     std::vector<int32_t> tmp((size_t)m_);
     for (size_t i = 0; i < tmp.size(); ++i) {
         if (in[i] < 0 || in[i] >= task_.episode_len)
@@ -1042,6 +1078,7 @@ void Engine::set_step_counts_host(const int64_t* in) {
 
 void Engine::counters_host(uint64_t* rc, uint64_t* pc) {
     activate();
+    wait_device_face();
     uint64_t* r = fp64_ ? pd_->reset_ctr : pf_->reset_ctr;
     uint64_t* q = fp64_ ? pd_->param_ctr : pf_->param_ctr;
     if (rc) cuda_check(cudaMemcpyAsync(rc, r, (size_t)m_ * 8, cudaMemcpyDeviceToHost, stream_), "ctr D2H");
@@ -1053,6 +1090,7 @@ void Engine::counters_host(uint64_t* rc, uint64_t* pc) {
 // step kernel's wrench() in the engine precision
 void Engine::wrench_host(const double* act, double* out) {
     activate();
+    wait_device_face();
     ensure_staging();
     ensure_pack();
     const size_t N = (size_t)m_;
@@ -1065,6 +1103,7 @@ void Engine::wrench_host(const double* act, double* out) {
 
 void Engine::dr_factors_host(double* out) {
     activate();
+    wait_device_face();
     if (!ranges_.enabled) {
         for (int64_t e = 0; e < m_; ++e) {
             const BaseVehicle& v = veh_[0];
@@ -1166,9 +1205,33 @@ void Engine::restore(const void* in, size_t len) {
 
 void Engine::stats_host(double* out, bool clear) {
     activate();
+    wait_device_face();
     cuda_check(launch_stats_reduce(stats_part_, nstat_blk_, d_stats_out_, clear ? 1 : 0, stream_), "stats");
     cuda_check(cudaMemcpyAsync(out, d_stats_out_, NSTAT * 8, cudaMemcpyDeviceToHost, stream_), "stats D2H");
     cuda_check(cudaStreamSynchronize(stream_), "stats sync");
+}
+
+// ------------------------------------------------------------------ ordering
+// Host-ABI calls run on the engine's private stream; device-face work runs on
+// the caller's stream.  Each device-face launch records dev_ev_ on the caller's
+// stream (outside stream capture) and the next host-ABI call makes its stream
+// wait for it, so e.g. step_tensors(); states() needs no explicit synchronize.
+// (Host-ABI calls synchronize before they return, so the reverse order holds.)
+void Engine::note_device_face(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return;   // graph replays record at launch
+    cuda_check(cudaEventRecord(dev_ev_, st), "device-face event");
+    dev_pending_ = true;
+}
+
+void Engine::wait_device_face() {
+    if (!dev_pending_) return;
+    cuda_check(cudaStreamWaitEvent(stream_, dev_ev_, 0), "device-face wait");
+    dev_pending_ = false;
 }
 
 // ------------------------------------------------------------------ device face
@@ -1192,6 +1255,7 @@ void Engine::dev_step(const void* act, void* obs, void* rew, uint8_t* done, int8
     else
         cuda_check(Launch<float>::step(*pf_, track, dr, fossen_, pair_, (const float*)act, (float*)obs,
                                        (float*)rew, done, reason, st), "dev_step");
+    note_device_face(st);
 }
 
 void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
@@ -1203,12 +1267,14 @@ void Engine::dev_reset(uint64_t seed, void* obs, cudaStream_t st) {
         pf_->seed = seed;
         cuda_check(Launch<float>::reset(*pf_, (float*)obs, st), "dev_reset");
     }
+    note_device_face(st);
 }
 
 void Engine::dev_observe(void* obs, cudaStream_t st) {
     check_device();
     if (fp64_) cuda_check(Launch<double>::observe(*pd_, (double*)obs, st), "dev_observe");
     else cuda_check(Launch<float>::observe(*pf_, (float*)obs, st), "dev_observe");
+    note_device_face(st);
 }
 
 void Engine::dev_set_done_f32(float* buf) {
@@ -1234,12 +1300,14 @@ void Engine::dev_pd_actions(const UuvPdGains& g, const void* ref6, void* act, cu
     else
         cuda_check(Launch<float>::pd_actions(*pf_, g, (const float*)ref6, (float*)act, st),
                    "dev_pd_actions");
+    note_device_face(st);
 }
 
 void Engine::dev_states(void* out, cudaStream_t st) {
     check_device();
     if (fp64_) cuda_check(Launch<double>::pack_states_t(*pd_, (double*)out, st), "dev_states");
     else cuda_check(Launch<float>::pack_states_t(*pf_, (float*)out, st), "dev_states");
+    note_device_face(st);
 }
 
 void Engine::dev_bench_actions(void* act, cudaStream_t st) {
@@ -1248,11 +1316,13 @@ void Engine::dev_bench_actions(void* act, cudaStream_t st) {
     cuda_check(launch_bench_actions(seed, env_offset_, (int)m_, n_act_,
                                     fp64_ ? nullptr : (float*)act,
                                     fp64_ ? (double*)act : nullptr, st), "bench_actions");
+    note_device_face(st);
 }
 
 void Engine::dev_stats(double* out, bool clear, cudaStream_t st) {
     check_device();
     cuda_check(launch_stats_reduce(stats_part_, nstat_blk_, out, clear ? 1 : 0, st), "dev_stats");
+    note_device_face(st);
 }
 
 void Engine::graph_capture(const void* act, void* obs, void* rew, uint8_t* done,
@@ -1282,6 +1352,7 @@ void Engine::graph_launch(cudaStream_t st) {
     check_device();
     if (!graph_exec_) throw RuntimeError("no captured graph (call uuvsim_dev_graph_capture first)");
     cuda_check(cudaGraphLaunch(graph_exec_, st), "GraphLaunch");
+    note_device_face(st);
 }
 
 void Engine::synchronize() {

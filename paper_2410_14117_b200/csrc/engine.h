@@ -111,6 +111,8 @@ public:
     std::string info() const;
     void activate() const;
     void check_device() const;
+    void note_device_face(cudaStream_t st);   // after a device-face launch
+    void wait_device_face();                  // before host-ABI work on stream_
 
 private:
     void parse(const std::string& text);
@@ -140,6 +142,7 @@ private:
     bool force_dense_ = false;
     bool band64_ = true;      // device.band64: fp64 recompute of steps entering the pitch band
     bool band_same_ = false;
+    bool band_tail_ = true;   // device.band_tail false: predictor misses stay fp32 (A/B only)
     double band_margin_ = -1e300;   // device.band_margin override (experiments; default by control_dt)  // device.band_stream "same": band kernel after the step, one stream
     int pair_mode_ = -1;      // device.pair: -1 auto, 0 off, 1 on
     int stage_mode_ = -1;     // device.stage_obs: -1 auto, 0 off, 1 on
@@ -169,6 +172,8 @@ private:
     int nstat_blk_ = 0;       // stats partial slots: step blocks + band blocks
     VehP<double>* d_veh64_ = nullptr;        // fp64 base vehicles (step-kernel tail)
     uint32_t* d_band_f_ = nullptr;           // band generation (2 words) + per-env flags
+    volatile int32_t* h_err_ = nullptr;      // rejected-resample flag (mapped page-locked)
+    volatile int32_t* d_err_ = nullptr;      // its device alias
     cudaStream_t band_side_ = nullptr;       // band kernel stream (fork / join per step)
     cudaEvent_t band_ev_[2] = {nullptr, nullptr};
     // ABI staging (f64 host layout; fp32 engines convert on device)
@@ -186,6 +191,8 @@ private:
     float4* d_vpack_ = nullptr;
     std::vector<VehP<double>> veh64_;   // fp64 base vehicles (band replay parameters)
     cudaStream_t stream_ = nullptr;
+    cudaEvent_t dev_ev_ = nullptr;   // last device-face launch (host-ABI calls wait for it)
+    bool dev_pending_ = false;
     cudaGraphExec_t graph_exec_ = nullptr;
     // host-ABI step replayed as one CUDA graph (H2D -> step -> D2H) while the
     // caller keeps passing the same page-locked buffers

@@ -219,6 +219,7 @@ template <class T> struct EngineP {
     V2<double>* dr64;      // [N][5] exact fp64 DR records (randomised fp32 engines)
     double sub_dt64;
     float band_theta;
+    float band_exit_theta; // = band_theta (device.band_tail = false: +inf, A/B only)
     float band_kdt;        // candidate predictor: control_dt
     float band_margin;     // candidate predictor margin (rad)
     int32_t band_per;      // envs scanned per band-kernel block (multiple of BLOCK)
@@ -239,6 +240,10 @@ template <class T> struct EngineP {
     // launching stream through these events (cudaStream_t / cudaEvent_t)
     void* band_side;
     void* band_ev[2];
+    // set (mapped page-locked word) when a per-episode DR resample is rejected
+    // (non-PD mass matrix): the host-ABI step then returns code 4 like the
+    // reference engine's panic (engine.rs:553-558, capi.rs:58-70)
+    volatile int32_t* err_flag;
 };
 
 constexpr int PACK_F4 = 10;   // 40 floats: Fossen pattern + restoring + trig constants

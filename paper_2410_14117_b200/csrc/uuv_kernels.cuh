@@ -197,7 +197,7 @@ __device__ __forceinline__ bool band_cand(const EngineP<float>& p, const float s
 // miss; p.s1[e].x is the step-initial theta, still in HBM): finished from an
 // fp64 recompute at the end of the step kernel (band_tail)
 __device__ __forceinline__ bool band_exit(const EngineP<float>& p, int e, float thmax) {
-    return thmax > p.band_theta && fabsf(p.s1[e].x) <= p.band_theta;
+    return thmax > p.band_exit_theta && fabsf(p.s1[e].x) <= p.band_theta;
 }
 
 // Reward / termination / auto-reset / stores / observation for one env whose
@@ -374,6 +374,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
                     p.dr0[e] = n0; p.dr1[e] = n1; p.dr2[e] = n2;
                 } else {
                     st.n_err += 1;
+                    if (p.err_flag) *p.err_flag = 1;   // host ABI: uuvsim_step reports code 4
                 }
                 p.param_ctr[e] = pc;
             }
@@ -902,24 +903,23 @@ struct BandP {
 
 constexpr int BAND_BLOCK = 128;        // band-kernel threads
 constexpr int BAND_SUB = 4 * 4 * BAND_BLOCK;   // flags scanned per pass: 4 uint4 per thread
-constexpr int BAND_LIST = 4096;        // candidate list capacity (shared memory)
 
 // Band kernel, launched on a side stream CONCURRENTLY with the step kernel
-// (which skips these envs).  Block b walks the chunks [b*band_per, ...) of the
-// batch: the chunk's flag words (EngineP::band_f) are read with 16-byte loads,
-// this step's candidates compacted into shared memory, and each stepped in fp64
-// -- recompute, reward / termination / reset / observation -- beside the fp32
-// step instead of after it.  Chunks are sized for about one pass of BAND_BLOCK
-// candidates: the band blocks are latency-bound (dependent fp64 chains), so
-// their number x lifetime is what they take from the step kernel's SMs.
-// Statistics go to the band kernel's own per-block partial slots.
+// (which skips these envs).  Block b owns chunk [b*band_per, (b+1)*band_per) of
+// the batch: the chunk's flag words (EngineP::band_f) are read with 16-byte
+// loads (no barrier between passes, so the passes' loads overlap), this step's
+// candidates compacted into a shared-memory list sized for the whole chunk, and
+// each stepped in fp64 -- recompute, reward / termination / reset / observation
+// -- beside the fp32 step instead of after it.  Statistics go to the band
+// kernel's own per-block partial slots.
+extern __shared__ __align__(16) int band_list[];
+
 template <bool TRACK, bool DR, bool MIX, class Pat>
 __global__ void __launch_bounds__(BAND_BLOCK)
 k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
     const EngineP<float>& p = bp.p;
-    __shared__ int list[BAND_LIST];
     __shared__ uint32_t cnt;
     const unsigned lane = threadIdx.x & 31;
     // this step's generation: envs the step kernel has already stepped carry the
@@ -927,60 +927,51 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
     const uint32_t gen = band_gen(p, p.band_ctr[1]);
     const uint32_t want = (gen << 1) | 1u;
     StatAcc st;
-    int scanned = 0;
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
-    auto drain = [&]() {   // step the listed candidates, empty the list
-        const uint32_t n = cnt;
-        for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
-            band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], list[i], gen, act, obs, rew,
-                                          done, reason, st);
-        __syncthreads();
-        if (threadIdx.x == 0) cnt = 0;
-        __syncthreads();
-    };
-    for (int cb = blockIdx.x * p.band_per; cb < p.n_env; cb += gridDim.x * p.band_per) {
-        const int cend = min(cb + p.band_per, p.n_env);
-        scanned += cend - cb;
-        for (int base = cb; base < cend; base += BAND_SUB) {
-            if (cnt + BAND_SUB > BAND_LIST) drain();   // uniform: cnt is read after a barrier
-            const int end = min(base + BAND_SUB, cend);
-            uint32_t f[16];
+    const int cb = blockIdx.x * p.band_per;
+    const int cend = min(cb + p.band_per, p.n_env);
+#pragma unroll 2
+    for (int base = cb; base < cend; base += BAND_SUB) {
+        const int end = min(base + BAND_SUB, cend);
+        uint32_t f[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = base + 4 * (threadIdx.x + k * BAND_BLOCK);
-                if (i + 3 < end) {
-                    const uint4 q = *reinterpret_cast<const uint4*>(p.band_f + i);
-                    f[4 * k] = q.x; f[4 * k + 1] = q.y; f[4 * k + 2] = q.z; f[4 * k + 3] = q.w;
-                } else {
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + 4 * (threadIdx.x + k * BAND_BLOCK);
+            if (i + 3 < end) {
+                const uint4 q = *reinterpret_cast<const uint4*>(p.band_f + i);
+                f[4 * k] = q.x; f[4 * k + 1] = q.y; f[4 * k + 2] = q.z; f[4 * k + 3] = q.w;
+            } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) f[4 * k + j] = i + j < end ? p.band_f[i + j] : 0u;
-                }
+                for (int j = 0; j < 4; ++j) f[4 * k + j] = i + j < end ? p.band_f[i + j] : 0u;
             }
-            uint32_t mine = 0;   // bit 4k+j: env base + 4 (t + k BAND_BLOCK) + j is a candidate
+        }
+        uint32_t mine = 0;   // bit 4k+j: env base + 4 (t + k BAND_BLOCK) + j is a candidate
 #pragma unroll
-            for (int j = 0; j < 16; ++j) mine |= (f[j] == want ? 1u : 0u) << j;
-            const uint32_t c = __popc(mine);
-            uint32_t incl = c;   // warp inclusive scan of the counts
+        for (int j = 0; j < 16; ++j) mine |= (f[j] == want ? 1u : 0u) << j;
+        const uint32_t c = __popc(mine);
+        uint32_t incl = c;   // warp inclusive scan of the counts
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (unsigned)o) incl += v;
-            }
-            uint32_t at = 0;
-            if (lane == 31 && incl) at = atomicAdd(&cnt, incl);
-            at = __shfl_sync(0xffffffffu, at, 31) + incl - c;
-            while (mine) {
-                const int j = __ffs(mine) - 1;
-                mine &= mine - 1;
-                list[at++] = base + 4 * (threadIdx.x + (j >> 2) * BAND_BLOCK) + (j & 3);
-            }
-            __syncthreads();
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += v;
+        }
+        uint32_t at = 0;
+        if (lane == 31 && incl) at = atomicAdd(&cnt, incl);
+        at = __shfl_sync(0xffffffffu, at, 31) + incl - c;
+        while (mine) {
+            const int j = __ffs(mine) - 1;
+            mine &= mine - 1;
+            band_list[at++] = base + 4 * (threadIdx.x + (j >> 2) * BAND_BLOCK) + (j & 3);
         }
     }
-    drain();
+    __syncthreads();
+    const uint32_t n = cnt;
+    for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
+        band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs, rew,
+                                      done, reason, st);
     if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
-    if (threadIdx.x == 0 && scanned > 0) atomicAdd(p.band_ctr + 1, (unsigned long long)scanned);
+    if (threadIdx.x == 0 && cend > cb) atomicAdd(p.band_ctr + 1, (unsigned long long)(cend - cb));
 }
 
 // band flags from the current states (after create / reset_all / set_states /
@@ -1412,6 +1403,17 @@ static cudaError_t launch_step_main(const EngineP<T>& p, bool track, bool dr, bo
     return cudaGetLastError();
 }
 
+template <auto KERNEL>
+static void allow_band_smem() {   // chunk lists beyond 48 KB (band_per up to 16,384 envs)
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4);
+    done.fetch_or(bit, std::memory_order_release);
+}
+
 // The band kernel on the engine's side stream, forked from and joined back to
 // the launching stream around the step kernel (fp32 engines with band64): it
 // runs the band candidates in fp64 while the step kernel runs everything else.
@@ -1431,7 +1433,12 @@ static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, boo
     q.stats = p.stats_band;
     const bool mix = p.n_veh > 1;
     const dim3 grid(std::max(1, p.band_grid));
-#define UUV_B(TR, D, M, PAT) k_band<TR, D, M, PAT><<<grid, BAND_BLOCK, 0, side>>>(bq, act, obs, rew, done, reason)
+    const size_t smem = (size_t)p.band_per * sizeof(int);   // candidate list for a whole chunk
+#define UUV_B(TR, D, M, PAT)                                                          \
+    do {                                                                              \
+        allow_band_smem<k_band<TR, D, M, PAT>>();                                     \
+        k_band<TR, D, M, PAT><<<grid, BAND_BLOCK, smem, side>>>(bq, act, obs, rew, done, reason); \
+    } while (0)
 #define UUV_BP(TR, D, M) \
     if (fossen) UUV_B(TR, D, M, PatFossen); else UUV_B(TR, D, M, PatDense)
     if (track) {
@@ -1459,14 +1466,15 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
         if (p.band_side && p.band_theta < INFINITY) {
             cudaStream_t side = (cudaStream_t)p.band_side;
             cudaEvent_t fork = (cudaEvent_t)p.band_ev[0], join = (cudaEvent_t)p.band_ev[1];
-            // the step kernel first: its blocks are dispatched first, the band
-            // kernel's few small blocks fill in beside them
+            // the band kernel first (high-priority stream): its blocks -- latency-
+            // bound fp64 chains -- start at once, the step kernel's waves fill
+            // the rest of the GPU around them
             cudaError_t e = cudaEventRecord(fork, st);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
-            if (e == cudaSuccess)
-                e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
             if (e == cudaSuccess) e = launch_band(p, track, dr, fossen, act, obs, rew, done, reason, side);
             if (e == cudaSuccess) e = cudaEventRecord(join, side);
+            if (e == cudaSuccess)
+                e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
             return e;
         }

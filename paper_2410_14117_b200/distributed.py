@@ -35,7 +35,9 @@ def shard_config(cfg: dict, rank: int, world: int, *, weak: bool = True) -> dict
     weak=True: every rank gets ``batch.num_envs`` envs (job size grows with N);
     weak=False: ``batch.num_envs`` is the job total, split into slabs.  Either
     way the global offset goes into ``batch.env_offset`` and a mixed-vehicle
-    ``batch.vehicle_mix`` keeps describing the whole job.
+    ``batch.vehicle_mix`` describes the whole job: under weak scaling the
+    per-vehicle counts (given for one slab's worth of envs) are scaled to the
+    grown job, so the vehicle proportions of the job are those of the config.
     """
     c = copy.deepcopy(cfg)
     b = c.setdefault("batch", {})
@@ -43,6 +45,12 @@ def shard_config(cfg: dict, rank: int, world: int, *, weak: bool = True) -> dict
     base_off = int(b.get("env_offset", 0))
     if weak:
         off, cnt = rank * n, n
+        mix = b.get("vehicle_mix")
+        if mix:
+            total = sum(int(x) for x in mix)
+            if total != n:
+                raise ValueError(f"batch.vehicle_mix sums to {total}, expected num_envs = {n}")
+            b["vehicle_mix"] = [int(x) * world for x in mix]
     else:
         off, cnt = shard_range(n, rank, world)
     b["num_envs"] = cnt

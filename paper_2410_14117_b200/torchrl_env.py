@@ -24,7 +24,6 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _core
 from .batch import B200EnvBatch
 
 REASON_TRUNCATED, REASON_DIVERGED, REASON_FAILED = 0, 1, 2
@@ -55,8 +54,7 @@ class VecEnv:
         self.dtype = batch.dtype
         self.final_obs = torch.zeros((self.num_envs, self.obs_dim), dtype=self.dtype,
                                      device=self.device)
-        _core.check(batch._lib, batch._lib.uuvsim_dev_set_final_obs(
-            batch._handle, self.final_obs.data_ptr(), self.final_obs.numel()))
+        batch.set_final_obs(self.final_obs)   # the batch keeps it alive while registered
         self._next = torch.empty_like(self.final_obs)
         self._term = torch.empty(self.num_envs, dtype=torch.bool, device=self.device)
         self._trunc = torch.empty_like(self._term)
@@ -78,8 +76,7 @@ class VecEnv:
 
     def close(self):
         if getattr(self.batch, "_open", False):
-            _core.check(self.batch._lib, self.batch._lib.uuvsim_dev_set_final_obs(
-                self.batch._handle, None, 0))
+            self.batch.set_final_obs(None)
         self.batch.close()
 
     def __enter__(self):

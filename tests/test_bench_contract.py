@@ -37,7 +37,7 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_gpu_arm_line():
-    d = _run("--steps", "20", "--warmup", "3", "--no-sweep")
+    d = _run("--steps", "20", "--warmup", "3", "--no-sweep", "--no-ncu")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
               "roofline", "cpu_baseline", "gpu_launches", "clocks"):
@@ -56,7 +56,11 @@ def test_gpu_arm_line():
         assert k in d["cpu_baseline"]
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"]
-    assert d["gpu_launches"] == 20
+    # the fused step kernel, plus the concurrent fp64 band kernel (band64 on)
+    assert d["gpu_launches"] == 20 * (2 if d["engine"]["band64"] else 1)
+    for k in ("per_env", "per_env_graph10"):
+        assert d["rtf"][k] > 0
+    assert d["cpu_baseline"]["one_thread"]["cores"] == 1 and d["cpu_baseline"]["cpu_model"]
 
 
 def test_reference_arm_under_torchrun_prints_once():
@@ -71,3 +75,27 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_gpu_arm_under_torchrun_two_ranks():
+    """The N > 1 path of the GPU arm (driver launch via torch.distributed.run):
+    two ranks on one device with the gloo backend -- weak-scaling headline,
+    max-over-ranks timing, the stats all-reduce and the C5 weak / strong
+    scaling block execute; rank 0 alone prints the line."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29533", str(ROOT / "bench.py"), "--gpus", "2",
+                        "--steps", "10", "--warmup", "3", "--dist-backend", "gloo",
+                        "--no-cpu", "--no-ncu"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["num_envs_total"] == 2 * d["config"]["num_envs_per_gpu"]
+    assert d["stats_allreduce_ms"] is not None
+    assert d["episode_stats"]["env_steps"] > 0
+    sc = d["scaling_c5"]
+    assert sc["weak"]["envs_total"] == 2 * (1 << 20) and sc["strong"]["envs_total"] == 1 << 20
+    assert sc["weak"]["value"] > 0 and sc["strong"]["value"] > 0

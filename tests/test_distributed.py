@@ -91,6 +91,8 @@ def test_shard_config_weak_and_strong():
     c = _cfg(100)
     w = shard_config(c, 3, 4, weak=True)
     assert w["batch"]["num_envs"] == 100 and w["batch"]["env_offset"] == 300
+    # weak scaling: the job grows to 400 envs with the config's vehicle proportions
+    assert w["batch"]["vehicle_mix"] == [4 * x for x in c["batch"]["vehicle_mix"]]
     s = shard_config(c, 3, 4, weak=False)
     assert s["batch"]["num_envs"] == 25 and s["batch"]["env_offset"] == 75
     assert s["batch"]["vehicle_mix"] == c["batch"]["vehicle_mix"]   # global mix kept
@@ -113,3 +115,61 @@ def test_gloo_world2_sharded_stats_match_single_process():
     assert np.array_equal(shard_states, whole_states)
     s = summarize(torch.tensor(reduced))
     assert s["episodes"] == reduced[1] + reduced[2] + reduced[3] > 0
+
+
+def _gpu_worker(rank, world, port, total, out_dir):
+    """One rank = one B200EnvBatch slab on cuda:0 (independent slabs, no kernel
+    waits on another rank); statistics all-reduced over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = shard_config(_cfg(total), rank, world, weak=False)
+    cfg["device"] = {"index": 0}
+    env = uuv.B200EnvBatch(cfg)
+    act = env.bench_actions_tensor()
+    env.stats(clear=True)
+    for _ in range(STEPS):
+        env.step_tensors(act)
+    torch.cuda.synchronize()
+    st = env.stats_tensor().cpu()
+    allreduce_stats(st)
+    np.save(os.path.join(out_dir, f"states_{rank}.npy"), env.states())
+    if rank == 0:
+        np.save(os.path.join(out_dir, "stats.npy"), st.numpy())
+    env.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_gloo_world2_b200_slabs_match_whole_batch():
+    """Sharding invariance on the engine itself: two ranks' env slabs (global
+    offsets, global vehicle mix) reproduce the unsharded B200 batch bit for bit,
+    and the all-reduced episode statistics equal the whole batch's."""
+    total, world = 6000, 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_gpu_worker, args=(world, _free_port(), total, d), nprocs=world,
+                           start_method="spawn")
+        reduced = np.load(os.path.join(d, "stats.npy"))
+        shard_states = np.concatenate([np.load(os.path.join(d, f"states_{r}.npy"))
+                                       for r in range(world)])
+    cfg = _cfg(total)
+    cfg["device"] = {"index": 0}
+    whole = uuv.B200EnvBatch(cfg)
+    act = whole.bench_actions_tensor()
+    whole.stats(clear=True)
+    for _ in range(STEPS):
+        whole.step_tensors(act)
+    torch.cuda.synchronize()
+    ws = whole.stats_tensor().cpu().numpy()
+    assert np.array_equal(shard_states, whole.states())
+    names = uuv.STAT_NAMES
+    for k, name in enumerate(names):
+        if name in ("sum_reward", "sum_episode_return"):
+            np.testing.assert_allclose(reduced[k], ws[k], rtol=1e-5)
+        else:
+            assert reduced[k] == ws[k], name
+    assert reduced[names.index("env_steps")] == total * STEPS
+    whole.close()

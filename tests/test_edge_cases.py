@@ -220,3 +220,67 @@ def test_host_staging_is_allocated_on_first_host_use():
         assert np.isfinite(obs).all()
     finally:
         lib.uuvsim_destroy(h)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(3600)
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck", "synccheck"])
+def test_compute_sanitizer_clean(tool):
+    """compute-sanitizer over every kernel family (tools/sanitize_run.py): the step
+    kernels incl. the concurrent fp64 band kernel and its in-kernel tail, the TMA
+    ring, host-ABI zero-copy / staged steps, fp64 engine, tcgen05 policy kernel."""
+    import shutil
+    import subprocess
+    import sys
+    from pathlib import Path
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not Path(cs).is_file():
+        pytest.skip("compute-sanitizer not found")
+    root = Path(__file__).resolve().parent.parent
+    extra = ["--racecheck-report", "all"] if tool == "racecheck" else []
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", *extra, sys.executable,
+                        str(root / "tools" / "sanitize_run.py")],
+                       capture_output=True, text=True, timeout=3500, cwd=root)
+    out = r.stdout + r.stderr
+    if "closed on this pool" in out:   # the GPU pool's wrapper refuses compute-sanitizer
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip()[:160])
+    log = root / "gpurun_out" / f"sanitizer_{tool}.log"
+    log.parent.mkdir(exist_ok=True)
+    log.write_text(out)
+    assert r.returncode == 0, out[-3000:]
+    assert "sanitize workload done" in out
+    assert "ERROR SUMMARY: 0 errors" in out, out[-2000:]
+
+
+@pytest.mark.gpu
+def test_rejected_episode_resample_is_runtime_error():
+    """A per-episode DR redraw whose M_RB + M_A is not positive definite: the
+    reference engine panics there (engine.rs:553-558), which its C ABI maps to
+    code 4 (capi.rs:58-70); uuvsim_step returns code 4 too.  The env keeps its
+    previous parameters and the device face counts the rejection in the stats.
+    (A heave added mass of -0.85 m keeps the base vehicle PD; with seed 2 the
+    create-time draw is PD and the first per-episode redraw is not -- found with
+    the oracle's sample_params.)"""
+    veh = uuv.default_params().to_dict()
+    am = [list(r) for r in veh["added_mass"]]
+    am[2][2] = -0.85 * veh["mass"]
+    veh["added_mass"] = am
+    ranges = uuv.RandomizationRanges(mass=(0.9, 1.1), added_mass=(0.5, 2.0), per_episode=True)
+    spec = uuv.TaskSpec(kind="station_keeping", episode_len=1)
+    cfg = uuv.engine_config_dict(veh, spec, 1, 2, 0, ranges, device=0)
+    env = uuv.B200EnvBatch(cfg)
+    before = env.dr_factors()
+    act = np.zeros((1, env.action_dim))
+    with pytest.raises(uuv.NativeError) as ei:
+        env.step(act)
+    assert ei.value.code == 4 and "not positive definite" in ei.value.message
+    assert np.array_equal(env.dr_factors(), before)          # previous parameters kept
+    env.close()
+    dev = uuv.B200EnvBatch(cfg)
+    import torch
+    a = torch.zeros((1, dev.action_dim), device="cuda")
+    dev.stats(clear=True)
+    dev.step_tensors(a)
+    torch.cuda.synchronize()
+    assert dev.stats()["resample_rejected"] == 1
+    dev.close()

@@ -2,6 +2,7 @@
 device time per step with and without band64 (for ncu: -k regex:k_band64)."""
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
 
@@ -13,16 +14,21 @@ import bench  # noqa: E402
 import paper_2410_14117_b200 as uuv  # noqa: E402
 
 
+FLUSH = os.environ.get("BAND_PROBE_FLUSH", "0") == "1"
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
     n_sub = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+    flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
     for band, stream, margin in ((True, "side", None), (True, "same", None), (True, "side", -10.0),
                                  (False, "side", None)):
         cfg, _ = bench.build_config(name, 0, "fp32", band64=band)
         cfg["device"]["band_stream"] = stream
         if margin is not None:
             cfg["device"]["band_margin"] = margin
+            cfg["device"]["band_tail"] = False
         cfg["task"]["n_substeps"] = n_sub
         cfg["task"]["control_dt"] = 0.005 * n_sub
         env = uuv.B200EnvBatch(cfg)
@@ -33,13 +39,25 @@ def main():
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         env.stats(clear=True)
-        a.record()
-        for _ in range(steps):
-            env.replay_graph()
-        b.record()
-        torch.cuda.synchronize()
+        if FLUSH:
+            tot = 0.0
+            for _ in range(steps):
+                flush.zero_()
+                a.record()
+                env.replay_graph()
+                b.record()
+                torch.cuda.synchronize()
+                tot += a.elapsed_time(b)
+            a_ms = tot
+        else:
+            a.record()
+            for _ in range(steps):
+                env.replay_graph()
+            b.record()
+            torch.cuda.synchronize()
+            a_ms = a.elapsed_time(b)
         st = env.stats()
-        print(name, "n_sub", n_sub, "band64", band, stream, "margin", margin, "us/step %.2f" % (a.elapsed_time(b) * 1e3 / steps),
+        print(name, "n_sub", n_sub, "band64", band, stream, "margin", margin, "us/step %.2f" % (a_ms * 1e3 / steps),
               "band steps/step %.1f" % (st["band64_steps"] / steps), flush=True)
         env.close()
 
