@@ -15,9 +15,6 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
-#ifdef UUV_BAND_CLOCK
-#include <cstdio>
-#endif
 
 #include <algorithm>
 #include <type_traits>
@@ -751,14 +748,8 @@ __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<dou
         a[k] = k >= nthr ? 0.0
                : p.io_f64 ? ((const double*)arow)[k]
                           : (double)((const float*)arow)[k];
-#ifdef UUV_BAND_CLOCK
-    const long long t0 = clock64() + (long long)(a[0] * 0.0 + in.s[0] * 0.0f);
-#endif
     const Band64Out r = slot1 ? replay_band64<DR, Pat>(p, V1, in.s, rec, a)
                               : replay_band64<DR, Pat>(p, V0, in.s, rec, a);
-#ifdef UUV_BAND_CLOCK
-    const long long t1 = clock64() + (long long)(r.v[0] * 0.0f);
-#endif
 #pragma unroll
     for (int k = 0; k < 12; ++k) in.s[k] = r.v[k];
     st.n_b64 += 1;
@@ -770,10 +761,6 @@ __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<dou
         finish_env<float, TRACK, DR, 0, Pat>(p, e, -1, g, in.s, in, r.failed != 0, obs, rew, done,
                                              reason, st);
     }
-#ifdef UUV_BAND_CLOCK
-    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 64))
-        printf("band_env t=%d replay %lld finish %lld\n", threadIdx.x, t1 - t0, clock64() - t1);
-#endif
 }
 
 // Step-kernel tail for a band-predictor miss (an env that was not a candidate
