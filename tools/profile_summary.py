@@ -4,8 +4,7 @@
         gpurun_out/prof_c5.ncu-rep:c5:1048576 ... [--launches gpurun_out/launches_c2.csv]
 
 Writes profiles/<tag>_ncu_summary.md (key metrics, executed-instruction mix
-per env-step, algorithmic vs executed FP32 work, dram traffic per env-step)
-and profiles/ncu_traffic.json (dram bytes per launch, read by bench.py).
+per env-step, algorithmic vs executed FP32 work, dram traffic per env-step).
 """
 
 from __future__ import annotations
@@ -90,21 +89,43 @@ def launch_share(path):
 def main():
     from bench import CONFIGS, bytes_per_env_step, flops_per_env_step
     ap = argparse.ArgumentParser()
-    ap.add_argument("reports", nargs="+", help="rep.ncu-rep:config:num_envs")
+    ap.add_argument("reports", nargs="+",
+                    help="rep.ncu-rep:config:num_envs[:band] (band: the fp64 band kernel)")
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--launches", action="append", default=[])
     a = ap.parse_args()
     out = [f"# ncu summary ({a.tag})", "",
-           "Captured with `ncu --set full --clock-control none --import-source on -k regex:k_step`"
-           " on one B200 (tools/ncu_run.sh).  ncu flushes caches and serialises launches, so"
-           " durations are cold-cache; bench.py's CUDA-event timings are the reported numbers.",
-           ""]
+           "Captured with `ncu --set full --clock-control none --import-source on` on one B200"
+           " (tools/ncu_run_r2.sh; step kernel `-k regex:k_step`, fp64 band kernel"
+           " `-k regex:k_band`, both after 300 steps in the tumbling regime).  ncu flushes"
+           " caches and serialises launches, so durations are cold-cache and the band kernel"
+           " is shown alone (in a step it runs concurrently with the step kernel);"
+           " bench.py's CUDA-event timings are the reported numbers.", ""]
     traffic = {}
     for spec in a.reports:
-        rep, cfg, n = spec.split(":")
+        parts = spec.split(":")
+        rep, cfg, n = parts[:3]
         n = int(n)
         v, u = raw(rep)
         c = CONFIGS[cfg]
+        if len(parts) > 3 and parts[3] == "band":
+            by = mix(rep)
+            out += [f"## {cfg} band kernel: {c['workload']}", "",
+                    f"report: `{Path(rep).name}`  kernel: `{v.get('Kernel Name', '?')[:90]}`", "",
+                    "| metric | value |", "|---|---|"]
+            for k, label in KEYS:
+                if k in v:
+                    out.append(f"| {label} (`{k}`) | {v[k]} {u.get(k, '')} |")
+            ex64 = 2 * by.get("DFMA", 0) + by.get("DMUL", 0) + by.get("DADD", 0)
+            tot = sum(by.values())
+            out += ["", f"* executed warp-instructions: {tot:.0f} (fp64 DFMA x2 + DMUL + DADD "
+                    f"warp-ops: {ex64:.0f}); the kernel scans {n} flag words and steps this "
+                    f"step's band candidates in fp64", "", "| opcode | warp-instructions |",
+                    "|---|---|"]
+            for k2, cnt in by.most_common(12):
+                out.append(f"| {k2} | {cnt:.0f} |")
+            out.append("")
+            continue
         name = [k for k in v if k == "Kernel Name"]
         out += [f"## {cfg}: {c['workload']}", "", f"report: `{Path(rep).name}`  kernel: "
                 f"`{v.get('Kernel Name', '?')[:90]}`", "", "| metric | value |", "|---|---|"]
@@ -151,7 +172,6 @@ def main():
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
     (prof / f"{a.tag}_ncu_summary.md").write_text("\n".join(out) + "\n")
-    (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print("\n".join(out))
 
 
