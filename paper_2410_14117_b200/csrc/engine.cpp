@@ -368,7 +368,8 @@ void Engine::parse(const std::string& text) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "side") band_same_ = false;
             else if (s == "same") band_same_ = true;
-            else throw ConfigError("device.band_stream must be \"side\" or \"same\"");
+            else if (s == "none") band_none_ = true;   // A/B: no band kernel (bookkeeping only)
+            else throw ConfigError("device.band_stream must be \"side\", \"same\" or \"none\"");
         }
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
@@ -519,7 +520,7 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.band_ctr = reinterpret_cast<unsigned long long*>(d_band_f_);   // 2 counters, then the flags
     p.band_f = d_band_f_ ? d_band_f_ + 64 : nullptr;
     p.band_inv_n = 1.0 / (double)m_;
-    p.band_side = band_same_ ? nullptr : band_side_;
+    p.band_side = (band_same_ || band_none_) ? nullptr : band_side_;
     p.band_same = band_same_ ? 1 : 0;
     p.band_ev[0] = band_ev_[0];
     p.band_ev[1] = band_ev_[1];
@@ -607,7 +608,7 @@ void Engine::allocate() {
     // band kernel: chunks of n/256 envs (2,048-8,192, a multiple of 2,048): a
     // few dozen candidates per block (one pass), spread over the SMs
     if (!fp64_ && band64_) {
-        const int64_t per = std::min<int64_t>(8192, std::max<int64_t>(2048, (m_ / 256 + 2047) / 2048 * 2048));
+        const int64_t per = std::min<int64_t>(4096, std::max<int64_t>(2048, (m_ / 256 + 2047) / 2048 * 2048));
         band_per_ = (int)per;
         band_grid_ = (int)((m_ + per - 1) / per);
     }

@@ -142,6 +142,7 @@ private:
     bool force_dense_ = false;
     bool band64_ = true;      // device.band64: fp64 recompute of steps entering the pitch band
     bool band_same_ = false;
+    bool band_none_ = false;  // device.band_stream "none": no band kernel at all (A/B only)
     bool band_tail_ = true;   // device.band_tail false: predictor misses stay fp32 (A/B only)
     double band_margin_ = -1e300;   // device.band_margin override (experiments; default by control_dt)  // device.band_stream "same": band kernel after the step, one stream
     int pair_mode_ = -1;      // device.pair: -1 auto, 0 off, 1 on

@@ -15,6 +15,35 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+// UUV_BAND_CLOCK (A/B builds only): per-block %globaltimer timeline of the step
+// and band kernels in a device table (row = event, column = block), read back
+// with uuvsim_debug_timeline (tools/band_timeline.py)
+#ifdef UUV_BAND_CLOCK
+constexpr int TL_BLOCKS = 8192;
+enum { TL_STEP_START, TL_STEP_END, TL_BAND_START, TL_BAND_SCAN, TL_BAND_END, TL_STEP_LOADED,
+       TL_STEP_SUBS, TL_BAND_LOADED, TL_BAND_REPLAYED, TL_BAND_GEN, TL_BAND_LOOP_CYC, TL_BAND_LOOP_N,
+       TL_ROWS };
+static __device__ unsigned long long g_uuv_tl[TL_ROWS][TL_BLOCKS];   // per TU (fp32 read back)
+__device__ __forceinline__ unsigned long long uuv_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define UUV_TL(row) \
+    do { if (threadIdx.x == 0 && blockIdx.x < TL_BLOCKS) g_uuv_tl[row][blockIdx.x] = uuv_gtimer(); } while (0)
+// stamp taken once `val` (a float) has arrived: the branch waits for it
+// (UUV_BAND_CLOCK=2 only: these in-kernel stamps perturb the fp64 replay's schedule)
+#if UUV_BAND_CLOCK >= 2
+#define UUV_TLV(row, val) \
+    do { if (threadIdx.x == 0 && blockIdx.x < TL_BLOCKS && __float_as_uint(val) != 0x7fc00001u) \
+             g_uuv_tl[row][blockIdx.x] = uuv_gtimer(); } while (0)
+#else
+#define UUV_TLV(row, val) do { } while (0)
+#endif
+#else
+#define UUV_TL(row) do { } while (0)
+#define UUV_TLV(row, val) do { } while (0)
+#endif
 
 #include <algorithm>
 #include <type_traits>
@@ -88,6 +117,37 @@ __device__ __forceinline__ void replay_env(const EngineP<float>& p, const VehP<f
 // Returns the state rounded to fp32 by value.  Used by the band kernel (k_band)
 // for predicted candidates and by the step kernel's out-of-line tail (band_tail)
 // for predictor misses.
+#ifndef UUV_BAND_REGE
+#define UUV_BAND_REGE 1
+#endif
+// Fossen-pattern fp64 vehicle constants copied into a register-resident
+// EnvParams (same values: substep_f64<true> with them is bit-identical to
+// substep_f64<false> on V), so the sub-step loop's DFMAs read registers instead
+// of ~40 kernel-parameter constants per sub-step
+__device__ __forceinline__ void reg_vehicle64(const VehP<double>& V, EnvParams<double, true>& R) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (PatFossen::M(i, j)) {
+                R.mtot[i * 6 + j] = V.mtot[i * 6 + j];
+                R.kdt[i * 6 + j] = V.kdt[i * 6 + j];
+            }
+        R.dq[i] = V.dquad[i];
+        R.dl[i] = V.dlin[i * 6 + i];
+    }
+    R.wb = V.wb;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) R.hm[i] = V.hm[i];
+    // opaque copies: the compiler cannot fold them back into constant operands
+#pragma unroll
+    for (int i = 0; i < 36; ++i)
+        if (PatFossen::M(i / 6, i % 6)) asm("" : "+d"(R.mtot[i]), "+d"(R.kdt[i]));
+#pragma unroll
+    for (int i = 0; i < 6; ++i) asm("" : "+d"(R.dq[i]), "+d"(R.dl[i]));
+    asm("" : "+d"(R.wb), "+d"(R.hm[0]), "+d"(R.hm[1]), "+d"(R.hm[2]));
+}
+
 struct Band64Out {
     float v[12];
     int failed;
@@ -108,10 +168,9 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
     const double dt = p.sub_dt64;
     EnvParams<double, DR> E;
     if constexpr (DR) {   // the env's exact fp64 record (written with its fp32 twin)
-        build_env<double, Pat>(V, V4<double>{rec[0].x, rec[0].y, rec[1].x, rec[1].y},
-                               V4<double>{rec[2].x, rec[2].y, rec[3].x, rec[3].y},
-                               V2<double>{rec[4].x, rec[4].y}, dt, E);
-        if constexpr (Pat::fossen) fossen_kdt<double>(E.mtot, dt, E.kdt);
+        build_env<double, Pat, Pat::fossen>(V, V4<double>{rec[0].x, rec[0].y, rec[1].x, rec[1].y},
+                                            V4<double>{rec[2].x, rec[2].y, rec[3].x, rec[3].y},
+                                            V2<double>{rec[4].x, rec[4].y}, dt, E);
     }
     double tau[6];
     wrench<double, DR, DR>(V, E, act, true, tau);
@@ -127,8 +186,25 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
         double t[12];
 #pragma unroll
         for (int i = 0; i < 12; ++i) t[i] = s[i];
+#if UUV_BAND_CLOCK >= 2
+        const long long c0 = clock64() + (long long)(t[4] * 0.0);
+#endif
+#if UUV_BAND_REGE
+        if constexpr (!DR) {   // the vehicle constants the sub-step reads, in registers
+            EnvParams<double, true> R;
+            reg_vehicle64(V, R);
+#pragma unroll 1
+            for (int k = 0; k < p.task.n_substeps; ++k) substep_f64<true, false>(V, R, t, tau, dt);
+        } else
+#endif
 #pragma unroll 1
         for (int k = 0; k < p.task.n_substeps; ++k) substep_f64<DR, false>(V, E, t, tau, dt);
+#if UUV_BAND_CLOCK >= 2
+        if (threadIdx.x == 0 && blockIdx.x < TL_BLOCKS && t[4] != 12345.0) {
+            g_uuv_tl[TL_BAND_LOOP_CYC][blockIdx.x] = clock64() - c0;
+            g_uuv_tl[TL_BAND_LOOP_N][blockIdx.x] = p.task.n_substeps;
+        }
+#endif
         if (f32_range12(t)) {
 #pragma unroll
             for (int i = 0; i < 12; ++i) s[i] = t[i];
@@ -455,7 +531,10 @@ __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint
         in.bk = band_gen(p, p.band_ctr[0]);
         if (in.bf != (in.bk << 1)) return ENV_BAND;
     }
-    if constexpr (!is_f64<T>()) prewrap(s);
+    if constexpr (!is_f64<T>()) {
+        UUV_TLV(TL_STEP_LOADED, s[4] + (float)in.step);
+        prewrap(s);
+    }
 
     // fp32: Fossen-pattern parameters in registers (UUV_PACK_CONSTS) or in the
     // constant bank (default: keeps FFMAs at two register reads)
@@ -497,6 +576,7 @@ __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint
             substep_fused<DR, Pat, false>(V, E, s, tau, dt, K);
             thm = fmaxf(thm, fabsf(s[4]));
         }
+        UUV_TLV(TL_STEP_SUBS, thm);
         if (band_exit(p, e, thm)) return ENV_TAIL;
         if (!all_finite12(s)) {
             failed = true;
@@ -525,6 +605,7 @@ __device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1
     if (p.band_f) in0.bk = in1.bk = band_gen(p, p.band_ctr[0]);
     const bool cand0 = p.band_f && in0.bf != (in0.bk << 1);
     const bool cand1 = p.band_f && in1.bf != (in1.bk << 1);
+    UUV_TLV(TL_STEP_LOADED, s0[4] + s1[4] + (float)in0.step);
     prewrap(s0);
     prewrap(s1);
     constexpr bool REG = UUV_PACK_CONSTS;
@@ -547,6 +628,7 @@ __device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1
         thm0 = fmaxf(thm0, fabsf(s0[4]));
         thm1 = fmaxf(thm1, fabsf(s1[4]));
     }
+    UUV_TLV(TL_STEP_SUBS, thm0 + thm1);
     // codes: candidates (decided on entry) belong to the band kernel, misses to
     // the fp64 tail; both computed here anyway (two lockstep chains)
     const int c0 = cand0 ? ENV_BAND : (band_exit(p, e0, thm0) ? ENV_TAIL : ENV_DONE);
@@ -748,8 +830,10 @@ __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<dou
         a[k] = k >= nthr ? 0.0
                : p.io_f64 ? ((const double*)arow)[k]
                           : (double)((const float*)arow)[k];
+    UUV_TLV(TL_BAND_LOADED, in.s[4] + (float)a[0] + (float)in.step);
     const Band64Out r = slot1 ? replay_band64<DR, Pat>(p, V1, in.s, rec, a)
                               : replay_band64<DR, Pat>(p, V0, in.s, rec, a);
+    UUV_TLV(TL_BAND_REPLAYED, r.v[4]);
 #pragma unroll
     for (int k = 0; k < 12; ++k) in.s[k] = r.v[k];
     st.n_b64 += 1;
@@ -813,6 +897,7 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
     pdl_enter(p.pdl != 0);
+    UUV_TL(TL_STEP_START);
     if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e = blockIdx.x * BLOCK + threadIdx.x;
     if (p.stage_act) {
@@ -835,6 +920,7 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
         if (code == ENV_TAIL) band_tail<TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason);
         band_count(p, blockIdx.x * BLOCK, BLOCK);
     }
+    UUV_TL(TL_STEP_END);
 }
 
 // Paired variant: block b covers envs [2*BLOCK*b, 2*BLOCK*(b+1)); thread t
@@ -845,6 +931,7 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
             void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
             int8_t* __restrict__ reason) {
     pdl_enter(p.pdl != 0);
+    UUV_TL(TL_STEP_START);
     if (p.stagger_ns) __nanosleep((unsigned)((long long)blockIdx.x * p.stagger_ns / gridDim.x));
     const int e0 = blockIdx.x * (2 * BLOCK) + threadIdx.x, e1 = e0 + BLOCK;
     if (p.stage_act) {
@@ -879,6 +966,7 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     if (c0 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
     if (c1 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
     band_count(p, blockIdx.x * (2 * BLOCK), 2 * BLOCK);
+    UUV_TL(TL_STEP_END);
 }
 
 // Kernel parameters of the band kernel: the step's block plus the fp64 base
@@ -888,7 +976,7 @@ struct BandP {
     VehP<double> veh[MAX_VEH];
 };
 
-constexpr int BAND_BLOCK = 128;        // band-kernel threads
+constexpr int BAND_BLOCK = 64;         // band-kernel threads
 constexpr int BAND_SUB = 4 * 4 * BAND_BLOCK;   // flags scanned per pass: 4 uint4 per thread
 
 // Band kernel, launched on a side stream CONCURRENTLY with the step kernel
@@ -907,12 +995,14 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
     const EngineP<float>& p = bp.p;
+    UUV_TL(TL_BAND_START);
     __shared__ uint32_t cnt;
     const unsigned lane = threadIdx.x & 31;
     // this step's generation: envs the step kernel has already stepped carry the
     // next one, candidates (never touched by it) this one with the flag bit set
     const uint32_t gen = band_gen(p, p.band_ctr[1]);
     const uint32_t want = (gen << 1) | 1u;
+    UUV_TLV(TL_BAND_GEN, (float)gen);
     StatAcc st;
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
@@ -954,11 +1044,13 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
     }
     __syncthreads();
     const uint32_t n = cnt;
+    UUV_TL(TL_BAND_SCAN);
     for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
         band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs, rew,
                                       done, reason, st);
     if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
     if (threadIdx.x == 0 && cend > cb) atomicAdd(p.band_ctr + 1, (unsigned long long)(cend - cb));
+    UUV_TL(TL_BAND_END);
 }
 
 // band flags from the current states (after create / reset_all / set_states /

@@ -23,7 +23,7 @@ def main():
     n_sub = int(sys.argv[3]) if len(sys.argv) > 3 else 10
     flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
     for band, stream, margin in ((True, "side", None), (True, "same", None), (True, "side", -10.0),
-                                 (False, "side", None)):
+                                 (True, "none", -10.0), (False, "side", None)):
         cfg, _ = bench.build_config(name, 0, "fp32", band64=band)
         cfg["device"]["band_stream"] = stream
         if margin is not None:
