@@ -364,6 +364,13 @@ void Engine::parse(const std::string& text) {
             if (!v->is_boolean()) throw ConfigError("device.band_tail must be a bool");
             band_tail_ = v->get<bool>();
         }
+        if (const json* v = opt(*d, "band_per")) band_per_cfg_ = v->get<int64_t>();   // A/B only
+        if (const json* v = opt(*d, "band_order")) {   // "band_first" | "main_first" (A/B)
+            std::string s = v->is_string() ? v->get<std::string>() : "";
+            if (s == "band_first") band_order_ = 0;
+            else if (s == "main_first") band_order_ = 1;
+            else throw ConfigError("device.band_order must be \"band_first\" or \"main_first\"");
+        }
         if (const json* v = opt(*d, "band_stream")) {   // "side" (concurrent) | "same" (A/B)
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "side") band_same_ = false;
@@ -518,10 +525,12 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.band_grid = band_grid_;
     p.stats_band = stats_part_ + (size_t)nblk_ * NSTAT;
     p.band_ctr = reinterpret_cast<unsigned long long*>(d_band_f_);   // 2 counters, then the flags
-    p.band_f = d_band_f_ ? d_band_f_ + 64 : nullptr;
+    p.band_f = d_band_f_ ? reinterpret_cast<uint8_t*>(d_band_f_) + 256 : nullptr;
     p.band_inv_n = 1.0 / (double)m_;
     p.band_side = (band_same_ || band_none_) ? nullptr : band_side_;
     p.band_same = band_same_ ? 1 : 0;
+    // step kernel first once the batch outgrows the band chain's latency
+    p.band_main_first = band_order_ == 1 ? 1 : 0;
     p.band_ev[0] = band_ev_[0];
     p.band_ev[1] = band_ev_[1];
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are
@@ -605,10 +614,11 @@ void Engine::allocate() {
     nblk_ = (int)((m_ + BLOCK - 1) / BLOCK);
     // per-block statistics partials: the step kernel's blocks, then the band
     // replay kernel's (fp32 engines with band64)
-    // band kernel: chunks of n/256 envs (2,048-8,192, a multiple of 2,048): a
-    // few dozen candidates per block (one pass), spread over the SMs
+    // band kernel: chunks of n/256 envs, 2,048 to BAND_MAX_PER (a multiple of
+    // 2,048): a few dozen candidates per block (one pass), spread over the SMs
     if (!fp64_ && band64_) {
-        const int64_t per = std::min<int64_t>(4096, std::max<int64_t>(2048, (m_ / 256 + 2047) / 2048 * 2048));
+        int64_t per = std::min<int64_t>(BAND_MAX_PER, std::max<int64_t>(2048, (m_ / 256 + 2047) / 2048 * 2048));
+        if (band_per_cfg_ > 0) per = std::min<int64_t>(BAND_MAX_PER, (band_per_cfg_ + 15) / 16 * 16);
         band_per_ = (int)per;
         band_grid_ = (int)((m_ + per - 1) / per);
     }
@@ -617,8 +627,9 @@ void Engine::allocate() {
     cuda_check(cudaMalloc(&stats_part_, (size_t)nstat_blk_ * NSTAT * sizeof(double)), "cudaMalloc(stats)");
     cuda_check(cudaMemset(stats_part_, 0, (size_t)nstat_blk_ * NSTAT * sizeof(double)), "cudaMemset(stats)");
     if (band_grid_ > 0) {
-        cuda_check(cudaMalloc(&d_band_f_, (size_t)m_ * 4 + 256), "cudaMalloc(band flags)");
-        cuda_check(cudaMemset(d_band_f_, 0, (size_t)m_ * 4 + 256), "cudaMemset(band flags)");
+        const size_t bytes = 256 + ((size_t)m_ + 15) / 16 * 16;   // counters, then one byte per env
+        cuda_check(cudaMalloc(&d_band_f_, bytes), "cudaMalloc(band flags)");
+        cuda_check(cudaMemset(d_band_f_, 0, bytes), "cudaMemset(band flags)");
         // highest priority: as step-kernel blocks retire, the band kernel's small
         // blocks take the freed room before the step kernel's next wave
         int lo = 0, hi = 0;

@@ -142,6 +142,8 @@ private:
     bool force_dense_ = false;
     bool band64_ = true;      // device.band64: fp64 recompute of steps entering the pitch band
     bool band_same_ = false;
+    int band_order_ = 0;      // device.band_order: 0 band kernel first, 1 step kernel first (A/B)
+    int64_t band_per_cfg_ = 0;   // device.band_per: envs per band-kernel block (A/B; 0 auto)
     bool band_none_ = false;  // device.band_stream "none": no band kernel at all (A/B only)
     bool band_tail_ = true;   // device.band_tail false: predictor misses stay fp32 (A/B only)
     double band_margin_ = -1e300;   // device.band_margin override (experiments; default by control_dt)  // device.band_stream "same": band kernel after the step, one stream
@@ -172,7 +174,7 @@ private:
     int band_per_ = 0;        // envs scanned per band-kernel block
     int nstat_blk_ = 0;       // stats partial slots: step blocks + band blocks
     VehP<double>* d_veh64_ = nullptr;        // fp64 base vehicles (step-kernel tail)
-    uint32_t* d_band_f_ = nullptr;           // band generation (2 words) + per-env flags
+    uint32_t* d_band_f_ = nullptr;           // band env counters (256 B) + per-env flag bytes
     volatile int32_t* h_err_ = nullptr;      // rejected-resample flag (mapped page-locked)
     volatile int32_t* d_err_ = nullptr;      // its device alias
     cudaStream_t band_side_ = nullptr;       // band kernel stream (fork / join per step)

@@ -45,6 +45,25 @@ constexpr int STEP_MIN_BLOCKS_F64 = UUV_STEP_MIN_BLOCKS_F64;
                                    // slow the running kernel more than the launch they save
 #endif
 
+// band kernel (uuv_kernels.cuh k_band): two warps per block, chunks of up to
+// 16 x BAND_VEC x BAND_BLOCK envs (one 16-byte flag load per thread and vector).
+// Measured (tools/band_probe.py, flushed, us per step C2 / C4 / C3 / C5): 64
+// threads 14.5 / 16.6 / 24.8 / 101; one warp per block capped at 128 registers
+// (to fit beside six 80-register paired step blocks) 17.2 / 20.8 / 30.3 / 108.
+#ifndef UUV_BAND_BLOCK
+#define UUV_BAND_BLOCK 64
+#endif
+#ifndef UUV_BAND_VEC
+#define UUV_BAND_VEC 4
+#endif
+#ifndef UUV_BAND_MIN_BLOCKS
+#define UUV_BAND_MIN_BLOCKS 1
+#endif
+constexpr int BAND_BLOCK = UUV_BAND_BLOCK;
+constexpr int BAND_VEC = UUV_BAND_VEC;
+constexpr int BAND_MIN_BLOCKS = UUV_BAND_MIN_BLOCKS;
+constexpr int BAND_MAX_PER = 16 * BAND_VEC * BAND_BLOCK;
+
 #ifndef UUV_PAIR_AUTO_MIN_ENVS
 #define UUV_PAIR_AUTO_MIN_ENVS 131072
 #endif

@@ -225,15 +225,18 @@ template <class T> struct EngineP {
     int32_t band_per;      // envs scanned per band-kernel block (multiple of BLOCK)
     int32_t band_grid;     // band-kernel blocks
     int32_t band_same;     // band kernel on the launching stream after the step (A/B only)
+    int32_t band_main_first;   // side stream: launch the step kernel before the band kernel
     double* stats_band;    // the band kernel's per-block statistics partials
-    // Band ownership per env and step (uuv_kernels.cuh k_band): flag word
-    // band_f[e] = generation << 1 | candidate, written by whichever kernel steps
-    // the env for the next step.  The step kernel steps env e iff band_f[e] ==
-    // gen << 1, the band kernel iff == gen << 1 | 1.  Each kernel derives gen from
-    // its own env counter (band_ctr[0] step kernel, [1] band kernel): every block
-    // adds its env count at its end, so a block reading the counter at its start
-    // sees k * n_env + (less than n_env) during step k -> gen = counter / n_env.
-    uint32_t* band_f;
+    // Band ownership per env and step (uuv_kernels.cuh k_band): flag byte
+    // band_f[e] = (generation mod 128) << 1 | candidate, written by whichever
+    // kernel steps the env for the next step.  The step kernel steps env e iff
+    // band_f[e] == word(gen, 0), the band kernel iff == word(gen, 1) (only the
+    // generations k and k + 1 ever meet, so 7 bits tell them apart).  Each kernel
+    // derives gen from its own env counter (band_ctr[0] step kernel, [1] band
+    // kernel): one thread per block claims the block's envs with a fetch-add,
+    // whose return value is k * n_env + (less than n_env) during step k, so
+    // gen = value / n_env.
+    uint8_t* band_f;
     unsigned long long* band_ctr;
     double band_inv_n;     // 1 / n_env
     // host-only: the band kernel runs on band_side, forked from / joined to the

@@ -300,12 +300,17 @@ __device__ __forceinline__ uint32_t band_gen(const EngineP<T>& p, unsigned long 
     return (uint32_t)k & 0x7fffffffu;
 }
 
+// flag byte of generation gen (EngineP::band_f)
+__device__ __forceinline__ uint32_t band_word(uint32_t gen, bool cand) {
+    return ((gen & 0x7fu) << 1) | (cand ? 1u : 0u);
+}
+
 template <class T, bool TRACK, bool RR = TRACK> struct EnvIn {
     static constexpr bool kRegRows = TRACK && RR;
     T s[12];
     int32_t step;
     float ep_ret;
-    uint32_t bf = 0;   // band flag word (fp32 engines with band64): generation << 1 | candidate
+    uint32_t bf = 0;   // band flag byte (fp32 engines with band64): band_word(generation, candidate)
     uint32_t bk = 0;   // this step's generation (band_gen)
     V4<T> rows[kRegRows ? LA_PRE + 1 : 1];   // traj[step+1 .. step+1+LA_PRE]
 };
@@ -462,9 +467,14 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     p.ep_ret[e] = er;
     p.step[e] = nstep;
     if constexpr (!is_f64<T>()) {   // next step's band decision, one generation on
+#ifndef UUV_AB_NOFLAGST
         if (p.band_f)
-            p.band_f[e] = (((in.bk + 1u) & 0x7fffffffu) << 1) |
-                          (band_cand(p, s) ? 1u : 0u);
+#ifdef UUV_AB_SAMEGEN   // A/B only: with UUV_AB_NOCOUNT, a constant generation
+            p.band_f[e] = (uint8_t)band_word(in.bk, band_cand(p, s) && false);
+#else
+            p.band_f[e] = (uint8_t)band_word(in.bk + 1u, band_cand(p, s));
+#endif
+#endif
     }
     p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
     p.s1[e] = V4<T>{s[4], s[5], s[6], s[7]};
@@ -514,12 +524,56 @@ __device__ __forceinline__ void load_state(const EngineP<T>& p, int e, T s[12]) 
 // band kernel (candidate), or left to this kernel's fp64 tail (band_tail).
 enum EnvCode { ENV_DONE = 0, ENV_BAND = 1, ENV_TAIL = 2 };
 
+// This step's band generation in the step kernels (EngineP::band_ctr).  One
+// thread per block claims the block's envs with a fetch-add on the step
+// kernel's counter -- the value it returns is the count before the block, so
+// gen = value / n_env -- issued at the block's start, its result published
+// through shared memory behind named barrier 1 once the block's env loads are
+// in flight.  One counter access per block (not one load per warp on a single
+// address) and no counter update at the block's end.
+//   mode BG_NONE: no band bookkeeping; BG_SYNC: publish + barrier here (every
+//   thread of the block passes exactly one BG_SYNC or band_gen_sync); BG_GIVEN:
+//   gen already known; BG_LOAD: per-thread counter load (persistent kernel,
+//   counted at its end by band_count).
+enum { BG_NONE = 0, BG_SYNC = 1, BG_GIVEN = 2, BG_LOAD = 3 };
+struct BandGen {
+    unsigned long long c = 0;   // fetch-add result (thread 0 of the block)
+    uint32_t gen = 0;
+    int mode = BG_NONE;
+};
+
+// block's fetch-add on the step counter (thread 0; the others get 0)
+__device__ __forceinline__ BandGen band_claim(const EngineP<float>& p, int first, int span) {
+    BandGen bg;
+    if (!p.band_f) return bg;
+    bg.mode = BG_SYNC;
+    if (threadIdx.x == 0) {
+        const int n = min(span, p.n_env - first);
+        bg.c = atomicAdd(p.band_ctr, (unsigned long long)max(n, 0));
+    }
+    return bg;
+}
+
+__device__ __forceinline__ uint32_t band_gen_sync(const EngineP<float>& p, const BandGen& bg) {
+    __shared__ uint32_t s_gen;
+    if (threadIdx.x == 0) s_gen = band_gen(p, bg.c);
+    asm volatile("barrier.sync 1, %0;" ::"r"((int)blockDim.x) : "memory");
+    return s_gen;
+}
+
+__device__ __forceinline__ uint32_t band_gen_of(const EngineP<float>& p, const BandGen& bg) {
+    if (bg.mode == BG_SYNC) return band_gen_sync(p, bg);
+    if (bg.mode == BG_GIVEN) return bg.gen;
+    return band_gen(p, p.band_ctr[0]);
+}
+
 // One env per thread (every precision / pattern / randomisation mode).
 template <class T, bool TRACK, bool DR, int SLOT, class Pat>
 __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint64_t g,
                                         const void* __restrict__ act, void* __restrict__ obs,
                                         void* __restrict__ rew, uint8_t* __restrict__ done,
-                                        int8_t* __restrict__ reason, StatAcc& st) {
+                                        int8_t* __restrict__ reason, StatAcc& st,
+                                        const BandGen& bg) {
     const VehP<T>& V = p.veh[SLOT];
     const TaskP<T>& tk = p.task;
     EnvIn<T, TRACK, !DR> in;
@@ -527,9 +581,11 @@ __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint
     T* s = in.s;
     // not this kernel's env this step: a band candidate (or already stepped by the
     // concurrent band kernel)
-    if (p.band_f) {
-        in.bk = band_gen(p, p.band_ctr[0]);
-        if (in.bf != (in.bk << 1)) return ENV_BAND;
+    if constexpr (!is_f64<T>()) {
+        if (bg.mode != BG_NONE) {
+            in.bk = band_gen_of(p, bg);
+            if (in.bf != band_word(in.bk, false)) return ENV_BAND;
+        }
     }
     if constexpr (!is_f64<T>()) {
         UUV_TLV(TL_STEP_LOADED, s[4] + (float)in.step);
@@ -596,15 +652,16 @@ __device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1
                                           EnvIn<float, TRACK, false>& in1, const void* act0,
                                           const void* act1, bool io_f64, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
-                                          int8_t* __restrict__ reason, StatAcc& st) {
+                                          int8_t* __restrict__ reason, StatAcc& st,
+                                          const BandGen& bg) {
     using Pat = PatFossen;
     const VehP<float>& V = p.veh[SLOT];
     const TaskP<float>& tk = p.task;
     float* s0 = in0.s;
     float* s1 = in1.s;
-    if (p.band_f) in0.bk = in1.bk = band_gen(p, p.band_ctr[0]);
-    const bool cand0 = p.band_f && in0.bf != (in0.bk << 1);
-    const bool cand1 = p.band_f && in1.bf != (in1.bk << 1);
+    if (bg.mode != BG_NONE) in0.bk = in1.bk = band_gen_of(p, bg);
+    const bool cand0 = bg.mode != BG_NONE && in0.bf != band_word(in0.bk, false);
+    const bool cand1 = bg.mode != BG_NONE && in1.bf != band_word(in1.bk, false);
     UUV_TLV(TL_STEP_LOADED, s0[4] + s1[4] + (float)in0.step);
     prewrap(s0);
     prewrap(s1);
@@ -651,12 +708,13 @@ __device__ __forceinline__ int step_pair(const EngineP<float>& p, int e0, int e1
                                           int li1,
                                           const void* __restrict__ act, void* __restrict__ obs,
                                           void* __restrict__ rew, uint8_t* __restrict__ done,
-                                          int8_t* __restrict__ reason, StatAcc& st) {
+                                          int8_t* __restrict__ reason, StatAcc& st,
+                                        const BandGen& bg) {
     EnvIn<float, TRACK, false> in0, in1;
     load_env<float, TRACK>(p, e0, in0);
     load_env<float, TRACK>(p, e1, in1);
     return pair_core<TRACK, SLOT>(p, e0, e1, li0, li1, in0, in1, act_row(p, act, e0),
-                                  act_row(p, act, e1), p.io_f64, obs, rew, done, reason, st);
+                                  act_row(p, act, e1), p.io_f64, obs, rew, done, reason, st, bg);
 }
 
 // Block-level episode statistics: warp reductions -> shared memory -> one
@@ -704,13 +762,14 @@ __device__ __forceinline__ void block_stats(double* __restrict__ part, const Sta
 template <class T, bool TRACK, bool DR, bool MIX, class Pat>
 __device__ __forceinline__ int one_env(const EngineP<T>& p, int e, int li, const void* act,
                                        void* obs, void* rew, uint8_t* done, int8_t* reason,
-                                       StatAcc& st) {
+                                       StatAcc& st, const BandGen& bg) {
     const uint64_t g = p.env_offset + (uint64_t)e;
     bool slot1 = false;
     if constexpr (MIX) slot1 = (int64_t)g >= p.mix_bound0;
-    if (!slot1) return step_env<T, TRACK, DR, 0, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+    if (!slot1)
+        return step_env<T, TRACK, DR, 0, Pat>(p, e, li, g, act, obs, rew, done, reason, st, bg);
     if constexpr (MIX)
-        return step_env<T, TRACK, DR, 1, Pat>(p, e, li, g, act, obs, rew, done, reason, st);
+        return step_env<T, TRACK, DR, 1, Pat>(p, e, li, g, act, obs, rew, done, reason, st, bg);
     return ENV_DONE;
 }
 
@@ -855,8 +914,11 @@ template <bool TRACK, bool DR, bool MIX, class Pat>
 __device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const void* act,
                                        void* obs, void* rew, uint8_t* done, int8_t* reason) {
     StatAcc st;
-    band_env<TRACK, DR, MIX, Pat>(p, p.veh64_dev[0], p.veh64_dev[1], e,
-                                  band_gen(p, p.band_ctr[0]), act, obs, rew, done, reason, st);
+    // this step's generation (mod 128, all band_word keeps) from the env's own
+    // flag byte, untouched this step: the step kernel's counter may already
+    // have moved on
+    band_env<TRACK, DR, MIX, Pat>(p, p.veh64_dev[0], p.veh64_dev[1], e, (uint32_t)p.band_f[e] >> 1,
+                                  act, obs, rew, done, reason, st);
     if (p.stats_on) {
         double* part = p.stats + (size_t)blockIdx.x * NSTAT;
         atomicAdd(part + ST_REWARD, (double)st.rew);
@@ -877,6 +939,9 @@ __device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const voi
 // step kernel's env counter (fire-and-forget; EngineP::band_ctr)
 // (after a barrier: every thread of the block is past its last counter read)
 __device__ __forceinline__ void band_count(const EngineP<float>& p, int first, int span) {
+#ifdef UUV_AB_NOCOUNT
+    return;   // A/B builds only (breaks the band protocol)
+#endif
     if (!p.band_f) return;
     __syncthreads();
     const int n = min(span, p.n_env - first);
@@ -906,8 +971,13 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
     }
     StatAcc st;
     int code = ENV_DONE;
-    if (e < p.n_env) code = one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done,
-                                                            reason, st);
+    BandGen bg;
+    if constexpr (!is_f64<T>()) bg = band_claim(p, blockIdx.x * BLOCK, BLOCK);
+    if (e < p.n_env) {
+        code = one_env<T, TRACK, DR, MIX, Pat>(p, e, threadIdx.x, act, obs, rew, done, reason, st, bg);
+    } else if constexpr (!is_f64<T>()) {
+        if (bg.mode == BG_SYNC) band_gen_sync(p, bg);
+    }
     pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
         __shared__ uint32_t skip[BLOCK / 32];
@@ -918,7 +988,6 @@ k_step(const __grid_constant__ EngineP<T> p, const void* __restrict__ act,
     if (p.stats_on) block_stats(p.stats, st);
     if constexpr (!is_f64<T>()) {
         if (code == ENV_TAIL) band_tail<TRACK, DR, MIX, Pat>(p, e, act, obs, rew, done, reason);
-        band_count(p, blockIdx.x * BLOCK, BLOCK);
     }
     UUV_TL(TL_STEP_END);
 }
@@ -944,15 +1013,20 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     const int sl1 = MIX && (int64_t)(p.env_offset + (uint64_t)e1) >= p.mix_bound0;
     const int l0 = threadIdx.x, l1 = threadIdx.x + BLOCK;
     int c0 = ENV_DONE, c1 = ENV_DONE;
+    BandGen bg = band_claim(p, blockIdx.x * (2 * BLOCK), 2 * BLOCK);
     if (a0 && a1 && sl0 == sl1) {
         int c = ENV_DONE;
-        if (sl0 == 0) c = step_pair<TRACK, 0>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
-        else if constexpr (MIX) c = step_pair<TRACK, 1>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st);
+        if (sl0 == 0) c = step_pair<TRACK, 0>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st, bg);
+        else if constexpr (MIX) c = step_pair<TRACK, 1>(p, e0, e1, l0, l1, act, obs, rew, done, reason, st, bg);
         c0 = c & 3;
         c1 = c >> 2;
-    } else {
-        if (a0) c0 = one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st);
-        if (a1) c1 = one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st);
+    } else {   // block-edge threads: generation first (one barrier per thread), then the envs
+        if (bg.mode == BG_SYNC) {
+            bg.gen = band_gen_sync(p, bg);
+            bg.mode = BG_GIVEN;
+        }
+        if (a0) c0 = one_env<float, TRACK, false, MIX, PatFossen>(p, e0, l0, act, obs, rew, done, reason, st, bg);
+        if (a1) c1 = one_env<float, TRACK, false, MIX, PatFossen>(p, e1, l1, act, obs, rew, done, reason, st, bg);
     }
     pdl_trigger_late(p.pdl != 0);
     if (p.stage_obs) {
@@ -965,7 +1039,6 @@ k_step_pair(const __grid_constant__ EngineP<float> p, const void* __restrict__ a
     if (p.stats_on) block_stats(p.stats, st);
     if (c0 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
     if (c1 == ENV_TAIL) band_tail<TRACK, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
-    band_count(p, blockIdx.x * (2 * BLOCK), 2 * BLOCK);
     UUV_TL(TL_STEP_END);
 }
 
@@ -976,21 +1049,19 @@ struct BandP {
     VehP<double> veh[MAX_VEH];
 };
 
-constexpr int BAND_BLOCK = 64;         // band-kernel threads
-constexpr int BAND_SUB = 4 * 4 * BAND_BLOCK;   // flags scanned per pass: 4 uint4 per thread
 
 // Band kernel, launched on a side stream CONCURRENTLY with the step kernel
 // (which skips these envs).  Block b owns chunk [b*band_per, (b+1)*band_per) of
-// the batch: the chunk's flag words (EngineP::band_f) are read with 16-byte
-// loads (no barrier between passes, so the passes' loads overlap), this step's
-// candidates compacted into a shared-memory list sized for the whole chunk, and
-// each stepped in fp64 -- recompute, reward / termination / reset / observation
-// -- beside the fp32 step instead of after it.  Statistics go to the band
-// kernel's own per-block partial slots.
+// the batch (band_per <= BAND_MAX_PER): the chunk's flag bytes (EngineP::band_f)
+// are read with 16-byte loads issued together with the generation counter --
+// one memory round trip -- this step's candidates compacted into a
+// shared-memory list, and each stepped in fp64 -- recompute, reward /
+// termination / reset / observation -- beside the fp32 step instead of after
+// it.  Statistics go to the band kernel's own per-block partial slots.
 extern __shared__ __align__(16) int band_list[];
 
 template <bool TRACK, bool DR, bool MIX, class Pat>
-__global__ void __launch_bounds__(BAND_BLOCK)
+__global__ void __launch_bounds__(BAND_BLOCK, BAND_MIN_BLOCKS)
 k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
        int8_t* __restrict__ reason) {
@@ -998,48 +1069,71 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
     UUV_TL(TL_BAND_START);
     __shared__ uint32_t cnt;
     const unsigned lane = threadIdx.x & 31;
-    // this step's generation: envs the step kernel has already stepped carry the
-    // next one, candidates (never touched by it) this one with the flag bit set
-    const uint32_t gen = band_gen(p, p.band_ctr[1]);
-    const uint32_t want = (gen << 1) | 1u;
-    UUV_TLV(TL_BAND_GEN, (float)gen);
-    StatAcc st;
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
     const int cb = blockIdx.x * p.band_per;
     const int cend = min(cb + p.band_per, p.n_env);
-#pragma unroll 2
-    for (int base = cb; base < cend; base += BAND_SUB) {
-        const int end = min(base + BAND_SUB, cend);
-        uint32_t f[16];
+    // the chunk's claim on the band counter (thread 0: fetch-add, the value
+    // before it gives the generation) and every flag byte of the chunk, all in
+    // flight at once
+    __shared__ uint32_t s_gen;
+    unsigned long long ctr = 0;
+    if (threadIdx.x == 0) ctr = atomicAdd(p.band_ctr + 1, (unsigned long long)max(cend - cb, 0));
+    uint4 q[BAND_VEC];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + 4 * (threadIdx.x + k * BAND_BLOCK);
-            if (i + 3 < end) {
-                const uint4 q = *reinterpret_cast<const uint4*>(p.band_f + i);
-                f[4 * k] = q.x; f[4 * k + 1] = q.y; f[4 * k + 2] = q.z; f[4 * k + 3] = q.w;
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) f[4 * k + j] = i + j < end ? p.band_f[i + j] : 0u;
-            }
+    for (int k = 0; k < BAND_VEC; ++k) {
+        const int i = cb + 16 * (threadIdx.x + k * BAND_BLOCK);
+        if (i + 15 < cend) {
+            q[k] = *reinterpret_cast<const uint4*>(p.band_f + i);
+        } else {
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            for (int j = 0; j < 16 && i + j < cend; ++j) w[j >> 2] |= (uint32_t)p.band_f[i + j] << (8 * (j & 3));
+            q[k] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        uint32_t mine = 0;   // bit 4k+j: env base + 4 (t + k BAND_BLOCK) + j is a candidate
+    }
+    if (threadIdx.x == 0) {
+        cnt = 0;
+        s_gen = band_gen(p, ctr);
+    }
+    __syncthreads();
+    // this step's generation: envs the step kernel has already stepped carry the
+    // next one, candidates (never touched by it) this one with the flag bit set;
+    // padding bytes past the chunk are 0 and never match (candidate bit clear)
+    const uint32_t gen = s_gen;
+    const uint32_t want = band_word(gen, true) * 0x01010101u;
+    UUV_TLV(TL_BAND_GEN, (float)gen);
+    StatAcc st;
+    uint32_t mine[BAND_VEC];   // bit j of mine[k]: env cb + 16 (t + k BAND_BLOCK) + j is a candidate
+    uint32_t c = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) mine |= (f[j] == want ? 1u : 0u) << j;
-        const uint32_t c = __popc(mine);
-        uint32_t incl = c;   // warp inclusive scan of the counts
+    for (int k = 0; k < BAND_VEC; ++k) {
+        const uint32_t w[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+        mine[k] = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (unsigned)o) incl += v;
+        for (int h = 0; h < 4; ++h) {
+            // bytes equal to want: zero bytes of w ^ want (exact per-byte test)
+            const uint32_t x = w[h] ^ want;
+            const uint32_t z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
+            // z has bit 8b+7 set for each matching byte b
+#pragma unroll
+            for (int b = 0; b < 4; ++b) mine[k] |= ((z >> (8 * b + 7)) & 1u) << (4 * h + b);
         }
-        uint32_t at = 0;
-        if (lane == 31 && incl) at = atomicAdd(&cnt, incl);
-        at = __shfl_sync(0xffffffffu, at, 31) + incl - c;
-        while (mine) {
-            const int j = __ffs(mine) - 1;
-            mine &= mine - 1;
-            band_list[at++] = base + 4 * (threadIdx.x + (j >> 2) * BAND_BLOCK) + (j & 3);
+        c += __popc(mine[k]);
+    }
+    uint32_t incl = c;   // warp inclusive scan of the counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += v;
+    }
+    uint32_t at = 0;
+    if (lane == 31 && incl) at = atomicAdd(&cnt, incl);
+    at = __shfl_sync(0xffffffffu, at, 31) + incl - c;
+#pragma unroll
+    for (int k = 0; k < BAND_VEC; ++k) {
+        uint32_t m = mine[k];
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            band_list[at++] = cb + 16 * (threadIdx.x + k * BAND_BLOCK) + j;
         }
     }
     __syncthreads();
@@ -1049,7 +1143,6 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
         band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs, rew,
                                       done, reason, st);
     if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
-    if (threadIdx.x == 0 && cend > cb) atomicAdd(p.band_ctr + 1, (unsigned long long)(cend - cb));
     UUV_TL(TL_BAND_END);
 }
 
@@ -1057,7 +1150,7 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
 // restore): generation = the band kernels' current one
 __device__ __forceinline__ void write_band_flag(const EngineP<float>& p, int e, const float s[12]) {
     if (p.band_f)
-        p.band_f[e] = (band_gen(p, p.band_ctr[0]) << 1) | (band_cand(p, s) ? 1u : 0u);
+        p.band_f[e] = (uint8_t)band_word(band_gen(p, p.band_ctr[0]), band_cand(p, s));
 }
 template <class T> __device__ __forceinline__ void write_band_flag(const EngineP<T>&, int, const T*) {}
 
@@ -1303,6 +1396,8 @@ __global__ void __launch_bounds__(BLOCK, TMA_MIN_BLOCKS)
 k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict__ act,
                 void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
                 int8_t* __restrict__ reason) {
+    BandGen bgl;   // persistent kernel: per-thread counter loads, counted at its end
+    if (p.band_f) bgl.mode = BG_LOAD;
     constexpr int TILE = 2 * BLOCK;
     __shared__ __align__(8) uint64_t mbar[2];
     const int A = p.act_dim;
@@ -1367,18 +1462,18 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
             int c = ENV_DONE;
             if (sl0 == 0)
                 c = pair_core<false, 0>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
-                                        reason, st);
+                                        reason, st, bgl);
             else if constexpr (MIX)
                 c = pair_core<false, 1>(p, e0, e1, -1, -1, in0, in1, r0, r1, false, obs, rew, done,
-                                        reason, st);
+                                        reason, st, bgl);
             c0 = c & 3;
             c1 = c >> 2;
         } else {   // vehicle-slab boundary inside the pair: one env at a time
             if constexpr (MIX) {
                 c0 = one_env<float, false, false, MIX, PatFossen>(p, e0, -1, act, obs, rew, done,
-                                                                  reason, st);
+                                                                  reason, st, bgl);
                 c1 = one_env<float, false, false, MIX, PatFossen>(p, e1, -1, act, obs, rew, done,
-                                                                  reason, st);
+                                                                  reason, st, bgl);
             }
         }
         if (c0 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
@@ -1391,9 +1486,9 @@ k_step_pair_tma(const __grid_constant__ EngineP<float> p, const void* __restrict
     if (tail0 < p.n_env && blockIdx.x == n_full % gridDim.x) {
         const int e0 = tail0 + threadIdx.x, e1 = e0 + BLOCK;
         const int c0 = e0 < p.n_env ? one_env<float, false, false, MIX, PatFossen>(
-                                          p, e0, -1, act, obs, rew, done, reason, st) : ENV_DONE;
+                                          p, e0, -1, act, obs, rew, done, reason, st, bgl) : ENV_DONE;
         const int c1 = e1 < p.n_env ? one_env<float, false, false, MIX, PatFossen>(
-                                          p, e1, -1, act, obs, rew, done, reason, st) : ENV_DONE;
+                                          p, e1, -1, act, obs, rew, done, reason, st, bgl) : ENV_DONE;
         if (c0 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e0, act, obs, rew, done, reason);
         if (c1 == ENV_TAIL) band_tail<false, false, MIX, PatFossen>(p, e1, act, obs, rew, done, reason);
     }
@@ -1449,7 +1544,7 @@ static cudaError_t launch_step_main(const EngineP<T>& p, bool track, bool dr, bo
     do {                                                                               \
         allow_smem<k_step_pair<TR, M>>();                                              \
         const cudaError_t le = launch_k(k_step_pair<TR, M>, grid, dim3(BLOCK), smem, st, \
-                                        p.pdl != 0, p, act, obs, rew, done, reason);    \
+                                        p.pdl != 0, p, act, obs, rew, done, reason); \
         if (le != cudaSuccess) return le;                                              \
     } while (0)
             if (track) { if (mix) UUV_P(true, true); else UUV_P(true, false); }
@@ -1465,7 +1560,7 @@ static cudaError_t launch_step_main(const EngineP<T>& p, bool track, bool dr, bo
     do {                                                                                     \
         allow_smem<k_step<T, TR, D, M, PAT>>();                                              \
         const cudaError_t le = launch_k(k_step<T, TR, D, M, PAT>, grid, dim3(BLOCK), smem, st, \
-                                        p.pdl != 0, p, act, obs, rew, done, reason);          \
+                                        p.pdl != 0, p, act, obs, rew, done, reason); \
         if (le != cudaSuccess) return le;                                                    \
     } while (0)
 #define UUV_LP(TR, D, M) \
@@ -1545,14 +1640,18 @@ cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fosse
         if (p.band_side && p.band_theta < INFINITY) {
             cudaStream_t side = (cudaStream_t)p.band_side;
             cudaEvent_t fork = (cudaEvent_t)p.band_ev[0], join = (cudaEvent_t)p.band_ev[1];
-            // the band kernel first (high-priority stream): its blocks -- latency-
-            // bound fp64 chains -- start at once, the step kernel's waves fill
-            // the rest of the GPU around them
+            // launch order: the second kernel starts ~1 us after the first.  Small
+            // batches launch the band kernel first -- its latency-bound fp64
+            // chains are the step's critical path; larger ones the step kernel
+            // (EngineP::band_main_first), whose waves are then the critical path
+            // and the band kernel's blocks fit around them
             cudaError_t e = cudaEventRecord(fork, st);
+            if (e == cudaSuccess && p.band_main_first)
+                e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
             if (e == cudaSuccess) e = launch_band(p, track, dr, fossen, act, obs, rew, done, reason, side);
             if (e == cudaSuccess) e = cudaEventRecord(join, side);
-            if (e == cudaSuccess)
+            if (e == cudaSuccess && !p.band_main_first)
                 e = launch_step_main<T>(p, track, dr, fossen, pair, act, obs, rew, done, reason, st);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
             return e;

@@ -15,6 +15,8 @@ import paper_2410_14117_b200 as uuv  # noqa: E402
 
 
 FLUSH = os.environ.get("BAND_PROBE_FLUSH", "0") == "1"
+EAGER = os.environ.get("BAND_PROBE_EAGER", "0") == "1"   # stream launches instead of the graph
+VARIANTS = os.environ.get("BAND_PROBE_VARIANTS", "side,same,side-10,none-10,off").split(",")
 
 
 def main():
@@ -22,10 +24,22 @@ def main():
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
     n_sub = int(sys.argv[3]) if len(sys.argv) > 3 else 10
     flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
-    for band, stream, margin in ((True, "side", None), (True, "same", None), (True, "side", -10.0),
-                                 (True, "none", -10.0), (False, "side", None)):
+    table = {"side": (True, "side", None), "same": (True, "same", None),
+             "side-10": (True, "side", -10.0), "none-10": (True, "none", -10.0),
+             "bandfirst": (True, "side", None, "band_first"),
+             "mainfirst": (True, "side", None, "main_first"),
+             "per4096": (True, "side", None, None, 4096), "per2048": (True, "side", None, None, 2048),
+             "off": (False, "side", None)}
+    for spec in (table[v] for v in VARIANTS):
+        band, stream, margin = spec[:3]
+        order = spec[3] if len(spec) > 3 else None
+        per = spec[4] if len(spec) > 4 else None
         cfg, _ = bench.build_config(name, 0, "fp32", band64=band)
         cfg["device"]["band_stream"] = stream
+        if order:
+            cfg["device"]["band_order"] = order
+        if per:
+            cfg["device"]["band_per"] = per
         if margin is not None:
             cfg["device"]["band_margin"] = margin
             cfg["device"]["band_tail"] = False
@@ -34,8 +48,9 @@ def main():
         env = uuv.B200EnvBatch(cfg)
         act = env.bench_actions_tensor()
         env.capture_graph(act, n_steps=1)
+        run = (lambda: env.step_tensors(act)) if EAGER else env.replay_graph
         for _ in range(300):          # into the tumbling regime
-            env.replay_graph()
+            run()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         env.stats(clear=True)
@@ -44,7 +59,7 @@ def main():
             for _ in range(steps):
                 flush.zero_()
                 a.record()
-                env.replay_graph()
+                run()
                 b.record()
                 torch.cuda.synchronize()
                 tot += a.elapsed_time(b)
@@ -52,12 +67,12 @@ def main():
         else:
             a.record()
             for _ in range(steps):
-                env.replay_graph()
+                run()
             b.record()
             torch.cuda.synchronize()
             a_ms = a.elapsed_time(b)
         st = env.stats()
-        print(name, "n_sub", n_sub, "band64", band, stream, "margin", margin, "us/step %.2f" % (a_ms * 1e3 / steps),
+        print(name, "eager" if EAGER else "graph", "n_sub", n_sub, "band64", band, stream, order or "", per or "", "margin", margin, "us/step %.2f" % (a_ms * 1e3 / steps),
               "band steps/step %.1f" % (st["band64_steps"] / steps), flush=True)
         env.close()
 
