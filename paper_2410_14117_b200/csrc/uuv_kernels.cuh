@@ -467,14 +467,7 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     p.ep_ret[e] = er;
     p.step[e] = nstep;
     if constexpr (!is_f64<T>()) {   // next step's band decision, one generation on
-#ifndef UUV_AB_NOFLAGST
-        if (p.band_f)
-#ifdef UUV_AB_SAMEGEN   // A/B only: with UUV_AB_NOCOUNT, a constant generation
-            p.band_f[e] = (uint8_t)band_word(in.bk, band_cand(p, s) && false);
-#else
-            p.band_f[e] = (uint8_t)band_word(in.bk + 1u, band_cand(p, s));
-#endif
-#endif
+        if (p.band_f) p.band_f[e] = (uint8_t)band_word(in.bk + 1u, band_cand(p, s));
     }
     p.s0[e] = V4<T>{s[0], s[1], s[2], s[3]};
     p.s1[e] = V4<T>{s[4], s[5], s[6], s[7]};
@@ -935,13 +928,10 @@ __device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const voi
     }
 }
 
-// this block's envs [first, first + span) are done with the step: advance the
-// step kernel's env counter (fire-and-forget; EngineP::band_ctr)
-// (after a barrier: every thread of the block is past its last counter read)
+// persistent TMA kernel (BG_LOAD): the block's envs [first, first + span) are done
+// with the step: advance the step kernel's env counter (fire-and-forget;
+// EngineP::band_ctr; after a barrier: every thread is past its last counter read)
 __device__ __forceinline__ void band_count(const EngineP<float>& p, int first, int span) {
-#ifdef UUV_AB_NOCOUNT
-    return;   // A/B builds only (breaks the band protocol)
-#endif
     if (!p.band_f) return;
     __syncthreads();
     const int n = min(span, p.n_env - first);

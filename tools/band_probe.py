@@ -29,6 +29,7 @@ def main():
              "bandfirst": (True, "side", None, "band_first"),
              "mainfirst": (True, "side", None, "main_first"),
              "per4096": (True, "side", None, None, 4096), "per2048": (True, "side", None, None, 2048),
+             "per8192": (True, "side", None, None, 8192),
              "off": (False, "side", None)}
     for spec in (table[v] for v in VARIANTS):
         band, stream, margin = spec[:3]

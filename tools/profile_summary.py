@@ -119,7 +119,7 @@ def main():
             ex64 = 2 * by.get("DFMA", 0) + by.get("DMUL", 0) + by.get("DADD", 0)
             tot = sum(by.values())
             out += ["", f"* executed warp-instructions: {tot:.0f} (fp64 DFMA x2 + DMUL + DADD "
-                    f"warp-ops: {ex64:.0f}); the kernel scans {n} flag words and steps this "
+                    f"warp-ops: {ex64:.0f}); the kernel scans {n} flag bytes and steps this "
                     f"step's band candidates in fp64", "", "| opcode | warp-instructions |",
                     "|---|---|"]
             for k2, cnt in by.most_common(12):
