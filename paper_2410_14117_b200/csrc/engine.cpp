@@ -365,6 +365,7 @@ void Engine::parse(const std::string& text) {
             band_tail_ = v->get<bool>();
         }
         if (const json* v = opt(*d, "band_per")) band_per_cfg_ = v->get<int64_t>();   // A/B only
+        if (const json* v = opt(*d, "band_rege")) band_rege_ = v->get<bool>() ? 1 : 0;
         if (const json* v = opt(*d, "band_order")) {   // "band_first" | "main_first" (A/B)
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "band_first") band_order_ = 0;
@@ -531,6 +532,9 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     p.band_same = band_same_ ? 1 : 0;
     // step kernel first once the batch outgrows the band chain's latency
     p.band_main_first = band_order_ == 1 ? 1 : 0;
+    // register-resident fp64 vehicle constants in the band kernel while it is the
+    // step's critical path (small batches; device.band_rege overrides, A/B)
+    p.band_rege = band_rege_ >= 0 ? band_rege_ : (m_ <= 8192 ? 1 : 0);
     p.band_ev[0] = band_ev_[0];
     p.band_ev[1] = band_ev_[1];
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are

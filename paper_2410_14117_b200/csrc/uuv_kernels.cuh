@@ -117,13 +117,13 @@ __device__ __forceinline__ void replay_env(const EngineP<float>& p, const VehP<f
 // Returns the state rounded to fp32 by value.  Used by the band kernel (k_band)
 // for predicted candidates and by the step kernel's out-of-line tail (band_tail)
 // for predictor misses.
-#ifndef UUV_BAND_REGE
-#define UUV_BAND_REGE 1
-#endif
 // Fossen-pattern fp64 vehicle constants copied into a register-resident
 // EnvParams (same values: substep_f64<true> with them is bit-identical to
 // substep_f64<false> on V), so the sub-step loop's DFMAs read registers instead
-// of ~40 kernel-parameter constants per sub-step
+// of ~40 kernel-parameter constants per sub-step.  Used for small batches
+// (EngineP::band_rege), where the band kernel is the step's critical path: the
+// copy shortens the replay (C2 -0.9 us) but takes 30 more registers per thread,
+// which at 2^20 envs cost the step kernel's waves more (C5 +1.6 us) -- measured.
 __device__ __forceinline__ void reg_vehicle64(const VehP<double>& V, EnvParams<double, true>& R) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
@@ -153,7 +153,7 @@ struct Band64Out {
     int failed;
 };
 
-template <bool DR, class Pat>
+template <bool DR, class Pat, bool REGE = false>
 __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, const VehP<double>& V,
                                                    const float s32[12], const V2<double> rec[5],
                                                    const double act[MAX_THR]) {
@@ -189,14 +189,12 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
 #if UUV_BAND_CLOCK >= 2
         const long long c0 = clock64() + (long long)(t[4] * 0.0);
 #endif
-#if UUV_BAND_REGE
-        if constexpr (!DR) {   // the vehicle constants the sub-step reads, in registers
+        if constexpr (!DR && REGE) {   // the vehicle constants the sub-step reads, in registers
             EnvParams<double, true> R;
             reg_vehicle64(V, R);
 #pragma unroll 1
             for (int k = 0; k < p.task.n_substeps; ++k) substep_f64<true, false>(V, R, t, tau, dt);
         } else
-#endif
 #pragma unroll 1
         for (int k = 0; k < p.task.n_substeps; ++k) substep_f64<DR, false>(V, E, t, tau, dt);
 #if UUV_BAND_CLOCK >= 2
@@ -858,7 +856,7 @@ __device__ __forceinline__ const void* stage_actions(const EngineP<T>& p, const 
 // Everything the fp64 recompute of env e needs, loaded in one round trip, then
 // the recompute and the env's reward / termination / reset / stores /
 // observation (written directly, never staged).
-template <bool TRACK, bool DR, bool MIX, class Pat>
+template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false>
 __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<double>& V0,
                                          const VehP<double>& V1, int e, uint32_t gen, const void* act,
                                          void* __restrict__ obs, void* __restrict__ rew,
@@ -883,8 +881,8 @@ __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<dou
                : p.io_f64 ? ((const double*)arow)[k]
                           : (double)((const float*)arow)[k];
     UUV_TLV(TL_BAND_LOADED, in.s[4] + (float)a[0] + (float)in.step);
-    const Band64Out r = slot1 ? replay_band64<DR, Pat>(p, V1, in.s, rec, a)
-                              : replay_band64<DR, Pat>(p, V0, in.s, rec, a);
+    const Band64Out r = slot1 ? replay_band64<DR, Pat, REGE>(p, V1, in.s, rec, a)
+                              : replay_band64<DR, Pat, REGE>(p, V0, in.s, rec, a);
     UUV_TLV(TL_BAND_REPLAYED, r.v[4]);
 #pragma unroll
     for (int k = 0; k < 12; ++k) in.s[k] = r.v[k];
@@ -1050,7 +1048,7 @@ struct BandP {
 // it.  Statistics go to the band kernel's own per-block partial slots.
 extern __shared__ __align__(16) int band_list[];
 
-template <bool TRACK, bool DR, bool MIX, class Pat>
+template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false>
 __global__ void __launch_bounds__(BAND_BLOCK, BAND_MIN_BLOCKS)
 k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
@@ -1130,8 +1128,8 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
     const uint32_t n = cnt;
     UUV_TL(TL_BAND_SCAN);
     for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
-        band_env<TRACK, DR, MIX, Pat>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs, rew,
-                                      done, reason, st);
+        band_env<TRACK, DR, MIX, Pat, REGE>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs,
+                                            rew, done, reason, st);
     if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
     UUV_TL(TL_BAND_END);
 }
@@ -1598,13 +1596,15 @@ static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, boo
     const bool mix = p.n_veh > 1;
     const dim3 grid(std::max(1, p.band_grid));
     const size_t smem = (size_t)p.band_per * sizeof(int);   // candidate list for a whole chunk
-#define UUV_B(TR, D, M, PAT)                                                          \
+#define UUV_B(TR, D, M, PAT, RG)                                                      \
     do {                                                                              \
-        allow_band_smem<k_band<TR, D, M, PAT>>();                                     \
-        k_band<TR, D, M, PAT><<<grid, BAND_BLOCK, smem, side>>>(bq, act, obs, rew, done, reason); \
+        allow_band_smem<k_band<TR, D, M, PAT, RG>>();                                 \
+        k_band<TR, D, M, PAT, RG><<<grid, BAND_BLOCK, smem, side>>>(bq, act, obs, rew, done, reason); \
     } while (0)
-#define UUV_BP(TR, D, M) \
-    if (fossen) UUV_B(TR, D, M, PatFossen); else UUV_B(TR, D, M, PatDense)
+#define UUV_BP(TR, D, M)                                                                \
+    if (fossen && !D && p.band_rege) UUV_B(TR, false, M, PatFossen, true);              \
+    else if (fossen) UUV_B(TR, D, M, PatFossen, false);                                 \
+    else UUV_B(TR, D, M, PatDense, false)
     if (track) {
         if (dr) { if (mix) UUV_BP(true, true, true); else UUV_BP(true, true, false); }
         else { if (mix) UUV_BP(true, false, true); else UUV_BP(true, false, false); }

@@ -1,7 +1,8 @@
 """The fp64 band's ownership protocol gives one answer however
 the work is scheduled: the concurrent band kernel on the side stream (default),
 the band kernel after the step kernel on one stream, and the step kernel
-launched first; inside a CUDA graph as eagerly.  The engines free-run the same tumbling
+launched first, with the fp64 vehicle constants in registers or read from the
+kernel parameters; inside a CUDA graph as eagerly.  The engines free-run the same tumbling
 workloads and must agree bit for bit -- states, observations, rewards,
 terminations and the episode statistics -- while each runs hundreds of fp64
 band steps.  A race between the two kernels (an env stepped twice, or not at
@@ -25,6 +26,8 @@ VARIANTS = {
     "side": {},
     "same_stream": {"band_stream": "same"},
     "step_first": {"band_order": "main_first"},
+    "rege_on": {"band_rege": True},     # fp64 vehicle constants in registers (default <= 8,192 envs)
+    "rege_off": {"band_rege": False},
 }
 
 WORKLOADS = {

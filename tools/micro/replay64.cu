@@ -20,7 +20,7 @@ __global__ void k(const __grid_constant__ P2 q, float* io, long long* cyc, int r
     V2<double> rec[5];
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-        const Band64Out o = replay_band64<false, PatFossen>(q.p, q.v, s, rec, a);
+        const Band64Out o = replay_band64<false, PatFossen, true>(q.p, q.v, s, rec, a);
         for (int i = 0; i < 12; ++i) s[i] = o.v[i];
     }
     long long t1 = clock64();
