@@ -570,6 +570,18 @@ __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint
     EnvIn<T, TRACK, !DR> in;
     load_env<T, TRACK>(p, e, in);
     T* s = in.s;
+    // the action row and the DR record too, issued before the band ownership check
+    // (which may wait for the block's counter claim) so every load of the step
+    // shares one memory round trip
+    T av[MAX_THR];
+    load_actions<T>(V, act_row(p, act, e), p.io_f64, av);
+    [[maybe_unused]] V4<T> d0, d1;
+    [[maybe_unused]] V2<T> d2;
+    if constexpr (DR) {
+        d0 = p.dr0[e];
+        d1 = p.dr1[e];
+        d2 = p.dr2[e];
+    }
     // not this kernel's env this step: a band candidate (or already stepped by the
     // concurrent band kernel)
     if constexpr (!is_f64<T>()) {
@@ -594,13 +606,9 @@ __device__ __forceinline__ int step_env(const EngineP<T>& p, int e, int li, uint
         load_pack(p.vpack + SLOT * PACK_F4, R);
         load_regs<Pat>(R, E, dt32, K);
     }
-    if constexpr (DR) {
-        const V4<T> d0 = p.dr0[e], d1 = p.dr1[e];
-        const V2<T> d2 = p.dr2[e];
-        build_env<T, Pat>(V, d0, d1, d2, (T)tk.sub_dt, E);
-    }
+    if constexpr (DR) build_env<T, Pat>(V, d0, d1, d2, (T)tk.sub_dt, E);
     T tau[6];
-    wrench<T, DR, REG>(V, E, act_row(p, act, e), p.io_f64, tau);
+    wrench_vals<T, DR, REG>(V, E, av, tau);
 
     bool failed = false;
     if constexpr (is_f64<T>()) {
@@ -650,6 +658,9 @@ __device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1
     const TaskP<float>& tk = p.task;
     float* s0 = in0.s;
     float* s1 = in1.s;
+    float av0[MAX_THR], av1[MAX_THR];   // before the band check (see step_env)
+    load_actions<float>(V, act0, io_f64, av0);
+    load_actions<float>(V, act1, io_f64, av1);
     if (bg.mode != BG_NONE) in0.bk = in1.bk = band_gen_of(p, bg);
     const bool cand0 = bg.mode != BG_NONE && in0.bf != band_word(in0.bk, false);
     const bool cand1 = bg.mode != BG_NONE && in1.bf != band_word(in1.bk, false);
@@ -666,8 +677,8 @@ __device__ __forceinline__ int pair_core(const EngineP<float>& p, int e0, int e1
         load_regs<Pat>(R, E, dt, K);
     }
     float tau0[6], tau1[6];
-    wrench<float, false, REG>(V, E, act0, io_f64, tau0);
-    wrench<float, false, REG>(V, E, act1, io_f64, tau1);
+    wrench_vals<float, false, REG>(V, E, av0, tau0);
+    wrench_vals<float, false, REG>(V, E, av1, tau1);
     float thm0 = 0.0f, thm1 = 0.0f;   // max |theta| over the sub-steps
 #pragma unroll 1
     for (int k = 0; k < tk.n_substeps; ++k) {
