@@ -379,6 +379,11 @@ void Engine::parse(const std::string& text) {
             else if (s == "none") band_none_ = true;   // A/B: no band kernel (bookkeeping only)
             else throw ConfigError("device.band_stream must be \"side\", \"same\" or \"none\"");
         }
+        // without a band kernel nobody would step the predicted candidates: "none"
+        // only measures the step kernel's bookkeeping, with the predictor off
+        if (band_none_ && !(band_margin_ >= -1e30 && band_margin_ < -1.0))
+            throw ConfigError("device.band_stream \"none\" (A/B only) needs device.band_margin < -1 "
+                              "(no band candidates)");
         if (const json* v = opt(*d, "pattern")) {
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "dense") force_dense_ = true;

@@ -128,6 +128,10 @@ BASE = uuv.engine_config_dict(uuv.default_params(), uuv.TaskSpec(), 16, 0)
      "M_RB + M_A is not positive definite"),
     (lambda c: c["device"].__setitem__("precision", "fp16"), "device.precision"),
     (lambda c: c["device"].__setitem__("host_io", "dma"), "device.host_io"),
+    (lambda c: c["device"].__setitem__("band_stream", "sideways"), "device.band_stream"),
+    (lambda c: c["device"].__setitem__("band_stream", "none"), "needs device.band_margin < -1"),
+    (lambda c: c["device"].__setitem__("band_order", "last"), "device.band_order"),
+    (lambda c: c["device"].__setitem__("band64", 1), "device.band64 must be a bool"),
     (lambda c: c.update(vehicles=[c["vehicle"], c["vehicle"]]), "vehicle_mix"),
 ])
 def test_config_errors_are_code_1(lib, mutate, needle):
