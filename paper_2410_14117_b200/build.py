@@ -82,6 +82,8 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         (objdir / "k_f32.o", [*common_nv, "-c", str(CSRC / "k_f32.cu")], [CSRC / "k_f32.cu"]),
         (objdir / "k_f64.o", [*common_nv, "-fmad=false", "-c", str(CSRC / "k_f64.cu")],
          [CSRC / "k_f64.cu"]),
+        (objdir / "k_band.o", [*common_nv, "-fmad=false", "-c", str(CSRC / "k_band.cu")],
+         [CSRC / "k_band.cu"]),
         (objdir / "rl_kernels.o", [*common_nv, "-c", str(CSRC / "rl_kernels.cu")],
          [CSRC / "rl_kernels.cu", INCLUDE / "uuvsim_rl.h"]),
     ]

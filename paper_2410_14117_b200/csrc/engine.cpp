@@ -366,6 +366,10 @@ void Engine::parse(const std::string& text) {
         }
         if (const json* v = opt(*d, "band_per")) band_per_cfg_ = v->get<int64_t>();   // A/B only
         if (const json* v = opt(*d, "band_rege")) band_rege_ = v->get<bool>() ? 1 : 0;
+        if (const json* v = opt(*d, "band_refop")) {
+            if (!v->is_boolean()) throw ConfigError("device.band_refop must be a bool");
+            band_refop_ = v->get<bool>() ? 1 : 0;
+        }
         if (const json* v = opt(*d, "band_order")) {   // "band_first" | "main_first" (A/B)
             std::string s = v->is_string() ? v->get<std::string>() : "";
             if (s == "band_first") band_order_ = 0;
@@ -540,6 +544,11 @@ template <class T> void Engine::fill_params(EngineP<T>& p) {
     // register-resident fp64 vehicle constants in the band kernel while it is the
     // step's critical path (small batches; device.band_rege overrides, A/B)
     p.band_rege = band_rege_ >= 0 ? band_rege_ : (m_ <= 8192 ? 1 : 0);
+    // reference-order band steps for long control steps (>= 0.1 s): there an env
+    // can pitch from inside the band to the clamp within one step, where the
+    // dynamics amplify rounding differences by ~1e11 and only the reference's own
+    // operation order agrees with it; device.band_refop overrides
+    p.band_refop = band_refop_ >= 0 ? band_refop_ : (task_.control_dt >= 0.1 - 1e-12 ? 1 : 0);
     p.band_ev[0] = band_ev_[0];
     p.band_ev[1] = band_ev_[1];
     // staged rows pay off for tracking rows (144 B); station rows (48 B) are

@@ -145,6 +145,7 @@ private:
     int band_order_ = 0;      // device.band_order: 0 band kernel first, 1 step kernel first (A/B)
     int64_t band_per_cfg_ = 0;   // device.band_per: envs per band-kernel block (A/B; 0 auto)
     int band_rege_ = -1;         // device.band_rege: -1 auto (<= 8,192 envs), 0 / 1 (A/B)
+    int band_refop_ = -1;        // device.band_refop: -1 auto (control_dt >= 0.1 s), 0 / 1
     bool band_none_ = false;  // device.band_stream "none": no band kernel at all (A/B only)
     bool band_tail_ = true;   // device.band_tail false: predictor misses stay fp32 (A/B only)
     double band_margin_ = -1e300;   // device.band_margin override (experiments; default by control_dt)  // device.band_stream "same": band kernel after the step, one stream

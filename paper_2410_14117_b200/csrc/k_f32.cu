@@ -1,4 +1,5 @@
 // fp32 instantiation of the engine kernels (the product path).
+#define UUV_F32_TU 1   // defines launch_band (the band kernel's FMA-formulation instantiations)
 #include "uuv_kernels.cuh"
 #include "uuv_common_kernels.cuh"
 

@@ -227,6 +227,7 @@ template <class T> struct EngineP {
     int32_t band_same;     // band kernel on the launching stream after the step (A/B only)
     int32_t band_main_first;   // side stream: launch the step kernel before the band kernel
     int32_t band_rege;     // band kernel keeps the fp64 vehicle constants in registers (small batches)
+    int32_t band_refop;    // band steps in the reference's operation order (long control steps)
     double* stats_band;    // the band kernel's per-block statistics partials
     // Band ownership per env and step (uuv_kernels.cuh k_band): flag byte
     // band_f[e] = (generation mod 128) << 1 | candidate, written by whichever

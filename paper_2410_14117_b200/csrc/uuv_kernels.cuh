@@ -153,7 +153,7 @@ struct Band64Out {
     int failed;
 };
 
-template <bool DR, class Pat, bool REGE = false>
+template <bool DR, class Pat, bool REGE = false, bool REFOP = false>
 __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, const VehP<double>& V,
                                                    const float s32[12], const V2<double> rec[5],
                                                    const double act[MAX_THR]) {
@@ -166,11 +166,17 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
         s[5] = wrap_pi64(s[5]);
     }
     const double dt = p.sub_dt64;
+    // REFOP (EngineP::band_refop): the reference's operation order (substep_ref,
+    // Cholesky solve) instead of the FMA formulation -- exact in k_band.cu, which
+    // is compiled with -fmad=false
+    constexpr bool refop = REFOP;
     EnvParams<double, DR> E;
     if constexpr (DR) {   // the env's exact fp64 record (written with its fp32 twin)
-        build_env<double, Pat, Pat::fossen>(V, V4<double>{rec[0].x, rec[0].y, rec[1].x, rec[1].y},
-                                            V4<double>{rec[2].x, rec[2].y, rec[3].x, rec[3].y},
-                                            V2<double>{rec[4].x, rec[4].y}, dt, E);
+        const V4<double> r0{rec[0].x, rec[0].y, rec[1].x, rec[1].y};
+        const V4<double> r1{rec[2].x, rec[2].y, rec[3].x, rec[3].y};
+        const V2<double> r2{rec[4].x, rec[4].y};
+        if (refop) build_env<double, Pat, false>(V, r0, r1, r2, dt, E);
+        else build_env<double, Pat, Pat::fossen>(V, r0, r1, r2, dt, E);
     }
     double tau[6];
     wrench<double, DR, DR>(V, E, act, true, tau);
@@ -181,8 +187,8 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
     // Fossen path runs every sub-step unchecked and tests the final state; only
     // a failed step is re-run from the start with a check after each sub-step
     // (keeping the last good state), like the fp32 kernel's replay_env.
-    bool checked = !Pat::fossen;
-    if constexpr (Pat::fossen) {
+    bool checked = !Pat::fossen || refop;
+    if (!checked) {
         double t[12];
 #pragma unroll
         for (int i = 0; i < 12; ++i) t[i] = s[i];
@@ -214,9 +220,9 @@ __device__ __forceinline__ Band64Out replay_band64(const EngineP<float>& p, cons
 #pragma unroll 1
         for (int k = 0; k < p.task.n_substeps; ++k) {
             bool ok;
-            if constexpr (Pat::fossen) {
+            if (Pat::fossen && !refop) {
                 ok = substep_f64<DR, true>(V, E, s, tau, dt);
-            } else {
+            } else {   // reference operation order (dense pattern, or band_refop)
                 double t[12];
 #pragma unroll
                 for (int i = 0; i < 12; ++i) t[i] = s[i];
@@ -867,7 +873,7 @@ __device__ __forceinline__ const void* stage_actions(const EngineP<T>& p, const 
 // Everything the fp64 recompute of env e needs, loaded in one round trip, then
 // the recompute and the env's reward / termination / reset / stores /
 // observation (written directly, never staged).
-template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false>
+template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false, bool REFOP = false>
 __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<double>& V0,
                                          const VehP<double>& V1, int e, uint32_t gen, const void* act,
                                          void* __restrict__ obs, void* __restrict__ rew,
@@ -892,8 +898,8 @@ __device__ __forceinline__ void band_env(const EngineP<float>& p, const VehP<dou
                : p.io_f64 ? ((const double*)arow)[k]
                           : (double)((const float*)arow)[k];
     UUV_TLV(TL_BAND_LOADED, in.s[4] + (float)a[0] + (float)in.step);
-    const Band64Out r = slot1 ? replay_band64<DR, Pat, REGE>(p, V1, in.s, rec, a)
-                              : replay_band64<DR, Pat, REGE>(p, V0, in.s, rec, a);
+    const Band64Out r = slot1 ? replay_band64<DR, Pat, REGE, REFOP>(p, V1, in.s, rec, a)
+                              : replay_band64<DR, Pat, REGE, REFOP>(p, V0, in.s, rec, a);
     UUV_TLV(TL_BAND_REPLAYED, r.v[4]);
 #pragma unroll
     for (int k = 0; k < 12; ++k) in.s[k] = r.v[k];
@@ -919,8 +925,13 @@ __device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const voi
     // this step's generation (mod 128, all band_word keeps) from the env's own
     // flag byte, untouched this step: the step kernel's counter may already
     // have moved on
-    band_env<TRACK, DR, MIX, Pat>(p, p.veh64_dev[0], p.veh64_dev[1], e, (uint32_t)p.band_f[e] >> 1,
-                                  act, obs, rew, done, reason, st);
+    const uint32_t gen = (uint32_t)p.band_f[e] >> 1;
+    if (p.band_refop)   // reference operation order (FMA-contracted in this translation unit)
+        band_env<TRACK, DR, MIX, Pat, false, true>(p, p.veh64_dev[0], p.veh64_dev[1], e, gen, act,
+                                                   obs, rew, done, reason, st);
+    else
+        band_env<TRACK, DR, MIX, Pat>(p, p.veh64_dev[0], p.veh64_dev[1], e, gen, act, obs, rew,
+                                      done, reason, st);
     if (p.stats_on) {
         double* part = p.stats + (size_t)blockIdx.x * NSTAT;
         atomicAdd(part + ST_REWARD, (double)st.rew);
@@ -1059,7 +1070,7 @@ struct BandP {
 // it.  Statistics go to the band kernel's own per-block partial slots.
 extern __shared__ __align__(16) int band_list[];
 
-template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false>
+template <bool TRACK, bool DR, bool MIX, class Pat, bool REGE = false, bool REFOP = false>
 __global__ void __launch_bounds__(BAND_BLOCK, BAND_MIN_BLOCKS)
 k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
        void* __restrict__ obs, void* __restrict__ rew, uint8_t* __restrict__ done,
@@ -1139,8 +1150,8 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
     const uint32_t n = cnt;
     UUV_TL(TL_BAND_SCAN);
     for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
-        band_env<TRACK, DR, MIX, Pat, REGE>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act, obs,
-                                            rew, done, reason, st);
+        band_env<TRACK, DR, MIX, Pat, REGE, REFOP>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act,
+                                                   obs, rew, done, reason, st);
     if (p.stats_on) block_stats<BAND_BLOCK>(p.stats, st);
     UUV_TL(TL_BAND_END);
 }
@@ -1591,9 +1602,14 @@ static void allow_band_smem() {   // chunk lists beyond 48 KB (band_per up to 16
 // the launching stream around the step kernel (fp32 engines with band64): it
 // runs the band candidates in fp64 while the step kernel runs everything else.
 // Stream-capturable (the fork / join become graph edges).
-static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, bool fossen,
-                               const void* act, void* obs, void* rew, uint8_t* done,
-                               int8_t* reason, cudaStream_t side) {
+// The band kernel's launch; REFOP instantiations live in k_band.cu (compiled with
+// -fmad=false, so the reference-order path rounds like the reference), the FMA
+// formulation's in k_f32.cu (contraction on: the -fmad=false build of it measured
+// C2 +0.6 us, C3 +1.9 us).
+template <bool RF>
+static cudaError_t launch_band_impl(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                                    const void* act, void* obs, void* rew, uint8_t* done,
+                                    int8_t* reason, cudaStream_t side) {
     thread_local BandP bq;   // host staging of the launch parameters (copied at launch)
     EngineP<float>& q = bq.p;
     q = p;
@@ -1609,8 +1625,8 @@ static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, boo
     const size_t smem = (size_t)p.band_per * sizeof(int);   // candidate list for a whole chunk
 #define UUV_B(TR, D, M, PAT, RG)                                                      \
     do {                                                                              \
-        allow_band_smem<k_band<TR, D, M, PAT, RG>>();                                 \
-        k_band<TR, D, M, PAT, RG><<<grid, BAND_BLOCK, smem, side>>>(bq, act, obs, rew, done, reason); \
+        allow_band_smem<k_band<TR, D, M, PAT, RG, RF>>();                             \
+        k_band<TR, D, M, PAT, RG, RF><<<grid, BAND_BLOCK, smem, side>>>(bq, act, obs, rew, done, reason); \
     } while (0)
 #define UUV_BP(TR, D, M)                                                                \
     if (fossen && !D && p.band_rege) UUV_B(TR, false, M, PatFossen, true);              \
@@ -1627,6 +1643,27 @@ static cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, boo
 #undef UUV_B
     return cudaGetLastError();
 }
+
+cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                        const void* act, void* obs, void* rew, uint8_t* done,
+                        int8_t* reason, cudaStream_t side);
+cudaError_t launch_band_refop(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                              const void* act, void* obs, void* rew, uint8_t* done,
+                              int8_t* reason, cudaStream_t side);
+#if defined(UUV_F32_TU)
+cudaError_t launch_band(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                        const void* act, void* obs, void* rew, uint8_t* done,
+                        int8_t* reason, cudaStream_t side) {
+    if (p.band_refop) return launch_band_refop(p, track, dr, fossen, act, obs, rew, done, reason, side);
+    return launch_band_impl<false>(p, track, dr, fossen, act, obs, rew, done, reason, side);
+}
+#elif defined(UUV_BAND_TU)
+cudaError_t launch_band_refop(const EngineP<float>& p, bool track, bool dr, bool fossen,
+                              const void* act, void* obs, void* rew, uint8_t* done,
+                              int8_t* reason, cudaStream_t side) {
+    return launch_band_impl<true>(p, track, dr, fossen, act, obs, rew, done, reason, side);
+}
+#endif
 
 template <class T>
 cudaError_t Launch<T>::step(const EngineP<T>& p, bool track, bool dr, bool fossen, bool pair,
