@@ -119,7 +119,13 @@ def test_dr_factors(name):
     np.testing.assert_allclose(g, P.f32(want), rtol=2.5e-7, atol=0)
 
 
-@pytest.mark.parametrize("name", list(CONFIGS))
+# the long-control-step config at a size where envs pitch from inside the band to
+# the clamp within one step (chaotic: the band runs them in the reference's
+# operation order, EngineP::band_refop)
+STRICT_EXTRA = {"station_20sub_target_64k": dict(CONFIGS["station_20sub_target"], n=65536)}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS) + list(STRICT_EXTRA))
 def test_single_step_teacher_forced(name):
     """Strict single-step contract (BASELINE.json north_star).
 
@@ -134,7 +140,7 @@ def test_single_step_teacher_forced(name):
     terminations and reasons bit-exact (divergence-radius ties excluded and
     counted); observations = the oracle's observe() at the GPU state.
     """
-    cfg = _cfg(**CONFIGS[name])
+    cfg = _cfg(**(CONFIGS.get(name) or STRICT_EXTRA[name]))
     gpu = uuv.B200EnvBatch(cfg)
     ref = orc.OracleBatch(cfg, threads=8)
     at_gpu = orc.OracleBatch(cfg)          # evaluates observe() at the GPU state
