@@ -50,6 +50,16 @@ __device__ __forceinline__ unsigned long long uuv_gtimer() {
 
 #include "uuv_model.cuh"
 #include "launch.h"
+
+// UUV_BOUNDS_CHECK (checking builds only, tools/bounds_run.py): device-side
+// bounds asserts at the engine's computed indices -- env rows, band lists, flag
+// bytes, staged rows -- that trap on a violation.  compute-sanitizer is not
+// available on this GPU pool; the test suite runs against this build instead.
+#ifdef UUV_BOUNDS_CHECK
+#define UUV_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define UUV_CHECK(cond) do { } while (0)
+#endif
 #include "launch_kernel.cuh"
 
 namespace uuv {
@@ -327,6 +337,7 @@ __device__ __forceinline__ void load_env(const EngineP<T>& p, int e, EnvIn<T, TR
     in.s[8] = a2.x; in.s[9] = a2.y; in.s[10] = a2.z; in.s[11] = a2.w;
     in.step = p.step[e];
     in.ep_ret = p.ep_ret[e];
+    UUV_CHECK(e >= 0 && e < p.n_env);
     if (p.band_f) in.bf = p.band_f[e];
     if constexpr (TRACK) {
         const int tab_last = p.task.episode_len + p.task.lookahead;
@@ -483,11 +494,13 @@ __device__ __forceinline__ void finish_env(const EngineP<T>& p, int e, int li, u
     // contiguously afterwards (flush_obs); else straight to HBM
     const size_t D = (size_t)tk.obs_dim;
     if (p.io_f64) {
+        UUV_CHECK(e >= 0 && e < p.n_env && li < 2 * BLOCK);
         double* row = (p.stage_obs && li >= 0) ? (double*)uuv_smem + (size_t)li * D
                                                : (double*)obs + (size_t)e * D;
         write_obs<T, double, TRACK>(tk, row, s, in, nstep, pre);
         ((double*)rew)[e] = (double)reward;
     } else {
+        UUV_CHECK(e >= 0 && e < p.n_env && li < 2 * BLOCK);
         T* row = (p.stage_obs && li >= 0) ? (T*)uuv_smem + (size_t)li * D : (T*)obs + (size_t)e * D;
         write_obs<T, T, TRACK>(tk, row, s, in, nstep, pre);
         ((T*)rew)[e] = reward;
@@ -925,6 +938,7 @@ __device__ __noinline__ void band_tail(const EngineP<float>& p, int e, const voi
     // this step's generation (mod 128, all band_word keeps) from the env's own
     // flag byte, untouched this step: the step kernel's counter may already
     // have moved on
+    UUV_CHECK(e >= 0 && e < p.n_env);
     const uint32_t gen = (uint32_t)p.band_f[e] >> 1;
     if (p.band_refop)   // reference operation order (FMA-contracted in this translation unit)
         band_env<TRACK, DR, MIX, Pat, false, true>(p, p.veh64_dev[0], p.veh64_dev[1], e, gen, act,
@@ -961,6 +975,7 @@ __device__ __forceinline__ void band_count(const EngineP<float>& p, int first, i
 // rows this block did not finish (band candidates, tail envs), one bit per row
 __device__ __forceinline__ void mark_rows(uint32_t* mask, int row, bool skip) {
     const uint32_t b = __ballot_sync(0xffffffffu, skip);
+    UUV_CHECK(row >= 0 && row < 2 * BLOCK);
     if ((threadIdx.x & 31) == 0) mask[row >> 5] = b;
 }
 
@@ -1143,12 +1158,15 @@ k_band(const __grid_constant__ BandP bp, const void* __restrict__ act,
         while (m) {
             const int j = __ffs(m) - 1;
             m &= m - 1;
+            UUV_CHECK(at < (uint32_t)p.band_per);
+            UUV_CHECK(cb + 16 * (threadIdx.x + k * BAND_BLOCK) + j < cend);
             band_list[at++] = cb + 16 * (threadIdx.x + k * BAND_BLOCK) + j;
         }
     }
     __syncthreads();
     const uint32_t n = cnt;
     UUV_TL(TL_BAND_SCAN);
+    UUV_CHECK(n <= (uint32_t)p.band_per && p.band_per <= BAND_MAX_PER);
     for (uint32_t i = threadIdx.x; i < n; i += BAND_BLOCK)
         band_env<TRACK, DR, MIX, Pat, REGE, REFOP>(p, bp.veh[0], bp.veh[1], band_list[i], gen, act,
                                                    obs, rew, done, reason, st);

@@ -140,7 +140,7 @@ def test_single_step_teacher_forced(name):
     terminations and reasons bit-exact (divergence-radius ties excluded and
     counted); observations = the oracle's observe() at the GPU state.
     """
-    cfg = _cfg(**(CONFIGS.get(name) or STRICT_EXTRA[name]))
+    cfg = _cfg(**(CONFIGS[name] if name in CONFIGS else STRICT_EXTRA[name]))
     gpu = uuv.B200EnvBatch(cfg)
     ref = orc.OracleBatch(cfg, threads=8)
     at_gpu = orc.OracleBatch(cfg)          # evaluates observe() at the GPU state
